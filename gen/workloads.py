@@ -223,3 +223,17 @@ def random_lists(rng: np.random.Generator, n_lists: int, max_len: int, bits: int
         m = rng.random(n) < spike
         v[m] = rng.integers(0, 1 << 32, int(m.sum()), dtype=np.uint64).astype(np.uint32)
     return Workload(f"random_{n_lists}x{max_len}_{bits}b", ln, v, False, -1)
+
+
+def checksum(list_n: np.ndarray, values: np.ndarray, list_base: int = 0):
+    """G7 shard-additive checksum of decoded values (verification, not the method):
+    (sum_l sum_i mix64(((l+base) << 32 | i) ^ (d_i * 0x9E3779B97F4A7C15)), sum d_i, sum n_l)
+    mod 2^64, mix64 = splitmix64."""
+    lid, idx, _ = _list_index(np.asarray(list_n, np.uint32))
+    d = np.asarray(values, np.uint64)
+    with np.errstate(over="ignore"):
+        key = ((lid.astype(np.uint64) + np.uint64(list_base)) << np.uint64(32)) | idx.astype(np.uint64)
+        h = splitmix64(key ^ ((d * np.uint64(0x9E3779B97F4A7C15)) & M64))
+        H = int(np.sum(h, dtype=np.uint64))
+        S = int(np.sum(d, dtype=np.uint64))
+    return (H, S, int(np.sum(np.asarray(list_n, np.uint64))))

@@ -1,0 +1,195 @@
+/*
+ * gc.h -- C ABI of the B200-native Group-format posting-list decoder.
+ *
+ * Operation (PAPER.md = arXiv 1502.01916):
+ *   A batch of posting lists, each encoded in one of the paper's Group formats
+ *   with the 4-way vertical layout (§2.1.2, §3.1) and the
+ *   control area stored apart from the data area, is decoded back to
+ *   exactly the stored uint32 integers ("decoders emit exactly n"):
+ *     - Group-Simple          §4   (Table III; decoding P:L262-267)
+ *     - Group-Scheme          §5   (Table IV; Eq.(1)-(2) P:L330, P:L338;
+ *                                   binary / complete-unary / incomplete-unary LDs P:L312-318)
+ *     - Group-AFOR            §6.1 (frames of {8,16,32} quads)
+ *     - Group-PFD             §6.2 (decode steps 1-3; exceptions overwrite
+ *                                   their slot)
+ *   gc_decode_dgaps additionally applies the inverse of the d-gap transform of
+ *   P:L57 §2.1.1: d_i = (d_{i-1} + g_i) mod 2^32, restarting at every list.
+ *
+ * The exact byte layout (every reading of a silent or garbled passage) is
+ * specified in DESIGN.md §3; it is the layout oracle/ encodes.
+ *
+ * Conventions
+ *   - All functions are plain C; no C++, CUDA-runtime or torch types cross this
+ *     boundary.  A CUDA stream is passed as `void*` (a cudaStream_t; NULL = the
+ *     legacy default stream).
+ *   - "device" pointers are CUDA global-memory pointers; "host" pointers are CPU
+ *     pointers.  The caller owns every buffer.  The decode functions never
+ *     allocate device memory and keep no global mutable state: calls on distinct
+ *     workspaces are reentrant.
+ *   - Decode functions validate their arguments on the host synchronously and
+ *     return a gc_status; all GPU work is enqueued asynchronously on the stream.
+ *     Errors found in the stream contents on the device never fault: they set
+ *     sticky GC_DEV_* bits in the workspace (read them with
+ *     gc_read_device_status).  The output of a batch with any such bit set is
+ *     unspecified, but no access ever leaves the buffers described by the batch.
+ */
+#ifndef GC_H
+#define GC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+typedef enum {
+  GC_OK = 0,
+  GC_ERR_INVALID_ARGUMENT = 1,   /* null/misaligned pointer, inconsistent sizes           */
+  GC_ERR_UNKNOWN_CODEC = 2,
+  GC_ERR_BAD_VARIANT = 3,        /* Group-Scheme variant byte, or PFD frame length       */
+  GC_ERR_WORKSPACE_TOO_SMALL = 4,
+  GC_ERR_UNSUPPORTED_DEVICE = 5, /* not a compute-capability 10.x (sm_100a) device       */
+  GC_ERR_CUDA = 6,               /* a CUDA runtime call failed (launch, copy)            */
+  GC_ERR_NOT_INCREASING = 7,     /* encoder: delta requested on a non-increasing list    */
+  GC_ERR_NOMEM = 8               /* encoder: host allocation failed                      */
+} gc_status;
+
+/* Codec ids. */
+typedef enum { GC_GROUP_SIMPLE = 2, GC_GROUP_SCHEME = 3, GC_GROUP_AFOR = 4, GC_GROUP_PFD = 5 } gc_codec;
+
+/* Sticky device status bits, OR-ed by the kernels into the workspace. */
+enum {
+  GC_DEV_BAD_SELECTOR = 1u << 0,  /* Group-Simple selector nibble > 9 (Table III)               */
+  GC_DEV_BAD_LD = 1u << 1,        /* unary LD longer than 32/CG units; IU byte with no code     */
+  GC_DEV_BAD_FRAME = 1u << 2,     /* AFOR length code 3 or bit 7 set; PFD b not in 1..32,
+                                     wcode > 3                                                  */
+  GC_DEV_BAD_EXCEPTION = 1u << 3, /* PFD count > 4q, count>0 with wcode 0, position >= 4q or
+                                     not strictly increasing                                    */
+  GC_DEV_TRUNCATED = 1u << 4      /* a list needs control/data/exception bytes beyond its
+                                     [off, next_off) range, or the directory is inconsistent   */
+};
+
+/*
+ * A packed batch (layout in DESIGN.md §3.7).  The struct
+ * itself is host memory, read only during the call.  Arrays are DEVICE
+ * pointers for gc_decode / gc_decode_dgaps / gc_checksum and HOST pointers for
+ * gc_decode_host.
+ *
+ *   list_n[n_lists]        logical ints of each list (0 allowed)
+ *   ctrl_off[n_lists+1]    byte offset of each list's control area in ctrl;
+ *                          every offset is a multiple of 4 (one 32-bit control
+ *                          word never mixes two lists)
+ *   data_off[n_lists+1]    offset of each list's data area in data, in 128-bit
+ *                          vectors
+ *   exc_off[n_lists+1]     byte offset of each list's exception area (Group-PFD;
+ *                          may be NULL for other codecs)
+ *   out_off[n_lists+1]     exclusive prefix sum of list_n (int offsets into out)
+ *   ctrl, ctrl_bytes       control stream; 16-B aligned, ctrl_bytes % 16 == 0,
+ *                          ctrl_bytes >= ctrl_off[n_lists]
+ *   data, data_vectors     data stream of 128-bit vectors (component k of vector m
+ *                          is the little-endian u32 at byte 16m+4k); 16-B aligned
+ *   exc, exc_bytes         Group-PFD exception stream (positions then values per
+ *                          frame); 16-B aligned, exc_bytes % 16 == 0; NULL/0 for
+ *                          other codecs
+ *   total_out              = out_off[n_lists] = sum of list_n
+ *   variant                Group-Scheme: bits 0-1 log2 CG, bits 2-3 LD kind
+ *                          (0 binary, 1 complete unary, 2 incomplete unary; IU
+ *                          needs CG 4 or 8).  0 for other codecs.
+ *   pfd_frame_quads        Group-PFD frame length F in quadruples: 32 (default,
+ *                          128 ints, u8 positions) or 128 (512 ints, u16 LE
+ *                          positions).  Ignored by other codecs.
+ */
+typedef struct {
+  int32_t codec; /* gc_codec */
+  uint32_t variant;
+  uint32_t pfd_frame_quads;
+  uint32_t reserved;
+  uint64_t n_lists;
+  const uint32_t* list_n;
+  const uint64_t* ctrl_off;
+  const uint64_t* data_off;
+  const uint64_t* exc_off;
+  const uint64_t* out_off;
+  const uint8_t* ctrl;
+  uint64_t ctrl_bytes;
+  const void* data;
+  uint64_t data_vectors;
+  const uint8_t* exc;
+  uint64_t exc_bytes;
+  uint64_t total_out;
+} gc_batch;
+
+/* Bytes of device workspace gc_decode / gc_decode_dgaps need for this batch
+ * (tile descriptors, look-back words, counters, the status word).  Host only,
+ * no launch.  Returns GC_ERR_INVALID_ARGUMENT on a null argument. */
+gc_status gc_workspace_size(const gc_batch* b, uint64_t* bytes);
+
+/* Decode every list of the batch into out (DEVICE, 16-B aligned, total_out
+ * u32): out[out_off[l] + i] = the i-th integer of list l (the stored gaps or
+ * TFs).  ws: DEVICE workspace of >= gc_workspace_size bytes, 16-B aligned,
+ * exclusively owned by this call until the stream reaches it (it is reset
+ * inside the call).  Asynchronous on `stream`. */
+gc_status gc_decode(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes, void* stream);
+
+/* As gc_decode, then the per-list inclusive prefix sum mod 2^32 that turns
+ * d-gaps into docIDs, fused into the same pass. */
+gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          void* stream);
+
+/* Copy the sticky GC_DEV_* bits of a workspace to *host_bits.  Synchronises
+ * `stream`.  0 means the last decode on this workspace saw a well-formed batch. */
+gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream);
+
+/* Shard-additive checksum of a decoded batch (verification, never timed):
+ * dev_sum3[0] = sum_l sum_i mix64(((l+list_base) << 32 | i) ^ (out_i * 0x9E3779B97F4A7C15)),
+ * dev_sum3[1] = sum of out_i, dev_sum3[2] = sum of list_n, all mod 2^64
+ * (mix64 = the splitmix64 finaliser).  dev_sum3 is DEVICE
+ * memory (3 x u64), overwritten.  list_base is the global id of list 0. */
+gc_status gc_checksum(const gc_batch* b, const uint32_t* out, uint64_t list_base,
+                      uint64_t* dev_sum3, void* stream);
+
+/* End-to-end decode from HOST buffers: copies the directory and streams of
+ * `host_batch` (host pointers; pinned memory recommended) into `dev_scratch`,
+ * decodes (dgaps != 0: docIDs) and copies the result into host_out (total_out
+ * u32).  dev_scratch: DEVICE memory of >= gc_host_scratch_size bytes, 256-B
+ * aligned.  Asynchronous on `stream` (synchronise before reading host_out). */
+gc_status gc_host_scratch_size(const gc_batch* host_batch, uint64_t* bytes);
+gc_status gc_decode_host(const gc_batch* host_batch, uint32_t* host_out, int dgaps,
+                         void* dev_scratch, uint64_t scratch_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host encoder (multi-threaded C++; the bytes are identical to oracle/'s).
+ *   values[sum(list_n)]  HOST, concatenated lists; docIDs when delta != 0
+ *                        (each list strictly increasing; the encoder applies
+ *                        the d-gap of P:L57), else the integers to store.
+ *   zeta_num/zeta_den    Group-PFD exception threshold, default 1/10.
+ * gc_encode_begin encodes into encoder-owned host memory and fills the HOST
+ * directory arrays ctrl_off/data_off/exc_off/out_off [n_lists+1] and
+ * sizes[3] = {ctrl_bytes, data_vectors, exc_bytes} (ctrl/exc padded to 16 B).
+ * gc_encode_finish copies the streams into caller HOST buffers of those sizes
+ * and releases the handle (gc_encode_abort releases without copying).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t codec;
+  uint32_t variant;
+  uint32_t pfd_frame_quads;
+  uint32_t zeta_num;
+  uint32_t zeta_den;
+} gc_encode_params;
+
+gc_status gc_encode_begin(const gc_encode_params* p, const uint32_t* values,
+                          const uint32_t* list_n, uint64_t n_lists, int delta, int threads,
+                          uint64_t* ctrl_off, uint64_t* data_off, uint64_t* exc_off,
+                          uint64_t* out_off, uint64_t* sizes, void** handle);
+gc_status gc_encode_finish(void* handle, uint8_t* ctrl, void* data, uint8_t* exc);
+void gc_encode_abort(void* handle);
+
+const char* gc_status_string(gc_status s);
+int gc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC_H */

@@ -1,0 +1,330 @@
+// gc_codecs.cuh -- per-codec parsers of one 32-bit control word (sm_100a device code).
+//
+// Every list's control area starts 4-byte aligned, so a 32-bit
+// control word belongs to exactly one list.  For each codec a word is parsed on
+// its own (plus, for complete unary, the previous word of the same list) into the
+// "groups" whose control it owns, in stream order.  A group is the unit one
+// control pattern describes (§3.1: a pattern that described N ints now
+// describes N quadruples):
+//   Group-Simple  one 4-bit selector  -> NUM quads in one 128-bit vector (Table III)
+//   Group-Scheme  one length descriptor -> one quad at BW bits (Eq. (2))
+//   Group-AFOR    one header byte      -> a frame of 8/16/32 quads at one bw
+//   Group-PFD     one 4-byte header    -> a frame of F quads at b bits + exceptions
+// Quad counts are "raw" (not clamped to the list end); the caller clamps with the
+// list's quad count Q, which is how padding groups are ignored.
+#pragma once
+#include <cstdint>
+
+#include "gc_device.cuh"
+
+namespace gcd {
+
+// One group, relative to the word's running prefix (quads, lane bits, exception bytes).
+struct Grp {
+  uint32_t q0;    // raw quad offset of the group within the word
+  uint32_t nq;    // raw quads the group covers
+  int32_t d0;     // first data lane-bit of the group, relative to the word's data prefix
+  uint32_t dlen;  // lane bits the group occupies
+  uint32_t bw;    // bits per value
+  uint32_t step;  // lane bits between consecutive quads of the group
+  uint32_t e0;    // exception bytes before the group (PFD)
+  uint32_t elen;  // exception bytes of the group (PFD)
+  uint32_t cnt;   // PFD exception count
+  uint32_t wb;    // PFD exception value bytes (1/2/4)
+  uint32_t err;   // GC_DEV_* bits, reported only if the group starts before the list end
+};
+
+struct WCtx {
+  uint32_t w;      // the control word (little-endian load of 4 control bytes)
+  uint32_t prev;   // previous control word of the same list (valid iff widx > 0)
+  uint64_t widx;   // word index within the list's control area
+  uint64_t Q;      // quads of the list
+};
+
+struct WAgg {
+  uint32_t q, d, e;  // raw quads, lane bits, exception bytes owned by the word
+};
+
+__device__ __forceinline__ Grp grp0() {
+  Grp g;
+  g.q0 = 0; g.nq = 0; g.d0 = 0; g.dlen = 0; g.bw = 1; g.step = 0;
+  g.e0 = 0; g.elen = 0; g.cnt = 0; g.wb = 0; g.err = 0;
+  return g;
+}
+
+// ---------------------------------------------------------------- Group-Simple
+// Table III, 6-bit fields packed into one constant each.
+constexpr uint64_t kGsNum = (32ull << 0) | (16ull << 6) | (10ull << 12) | (8ull << 18) |
+                            (6ull << 24) | (5ull << 30) | (4ull << 36) | (3ull << 42) |
+                            (2ull << 48) | (1ull << 54);
+constexpr uint64_t kGsBw = (1ull << 0) | (2ull << 6) | (3ull << 12) | (4ull << 18) |
+                           (5ull << 24) | (6ull << 30) | (8ull << 36) | (10ull << 42) |
+                           (16ull << 48) | (32ull << 54);
+
+__device__ __forceinline__ uint32_t gs_num(uint32_t s) {
+  return s <= 9 ? (uint32_t)(kGsNum >> (6 * s)) & 63u : 1u;
+}
+__device__ __forceinline__ uint32_t gs_bw(uint32_t s) {
+  return s <= 9 ? (uint32_t)(kGsBw >> (6 * s)) & 63u : 32u;
+}
+
+struct CodecGS {
+  static constexpr bool kExc = false;
+  static constexpr bool kNeedsPrev = false;
+  static constexpr bool kMultiQuad = true;   // a group may hold several quads
+  static constexpr bool kVectorGroups = true;
+  __device__ static WAgg agg(const WCtx& c) {
+    uint32_t q = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) q += gs_num((c.w >> (4 * k)) & 15u);  // low nibble first (A6)
+    return WAgg{q, 8u * 32u, 0u};
+  }
+  template <class F>
+  __device__ static void walk(const WCtx& c, F&& f) {
+    uint32_t q = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      uint32_t s = (c.w >> (4 * k)) & 15u;
+      Grp g = grp0();
+      g.q0 = q;
+      g.nq = gs_num(s);
+      g.d0 = 32 * k;       // one 128-bit vector per selector
+      g.dlen = 32;
+      g.bw = gs_bw(s);
+      g.step = g.bw;       // int t of the component at [t*BW, (t+1)*BW) (A7)
+      g.err = s > 9 ? GC_DEV_BAD_SELECTOR : 0u;
+      f(g);
+      q += g.nq;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- Group-Scheme, binary LD
+// Field packing (A18): CG=1 three 5-bit fields per 16-bit unit; CG=2 two 4-bit per
+// byte; CG=4 two 3-bit per byte; CG=8 four 2-bit per byte; LSB-first.
+template <int CG>
+struct CodecGscB {
+  static constexpr bool kExc = false;
+  static constexpr bool kNeedsPrev = false;
+  static constexpr bool kMultiQuad = false;
+  static constexpr bool kVectorGroups = false;
+  static constexpr int kFields = CG == 1 ? 6 : (CG == 8 ? 16 : 8);
+  __device__ static __forceinline__ uint32_t field(uint32_t w, int k) {
+    if (CG == 1) return (w >> (16 * (k / 3) + 5 * (k % 3))) & 31u;
+    if (CG == 2) return (w >> (4 * k)) & 15u;
+    if (CG == 4) return (w >> (8 * (k / 2) + 3 * (k % 2))) & 7u;
+    return (w >> (2 * k)) & 3u;
+  }
+  __device__ static WAgg agg(const WCtx& c) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int k = 0; k < kFields; k++) d += CG * (field(c.w, k) + 1);  // Eq. (2)
+    return WAgg{(uint32_t)kFields, d, 0u};
+  }
+  template <class F>
+  __device__ static void walk(const WCtx& c, F&& f) {
+    int32_t d = 0;
+#pragma unroll
+    for (int k = 0; k < kFields; k++) {
+      Grp g = grp0();
+      g.q0 = k;
+      g.nq = 1;
+      g.d0 = d;
+      g.bw = CG * (field(c.w, k) + 1);  // BW = CG*(LD+1)
+      g.dlen = g.bw;
+      f(g);
+      d += (int32_t)g.bw;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- Group-Scheme, complete unary
+// Codes are (LD-1) ones then a 0, read MSB-first (A15/A16) and may cross
+// bytes and words.  Each control bit stands for CG data bits per lane, so the data
+// offset of a code is CG x its start bit (closed form); a word owns the codes whose
+// terminating 0 it holds.
+template <int CG>
+struct CodecGscCU {
+  static constexpr bool kExc = false;
+  static constexpr bool kNeedsPrev = true;
+  static constexpr bool kMultiQuad = false;
+  static constexpr bool kVectorGroups = false;
+  __device__ static WAgg agg(const WCtx& c) {
+    return WAgg{(uint32_t)__popc(~c.w), (uint32_t)(CG * 32), 0u};
+  }
+  template <class F>
+  __device__ static void walk(const WCtx& c, F&& f) {
+    uint32_t s = __byte_perm(c.w, 0, 0x0123);  // stream order: bit 31 = first bit
+    int32_t start = 0;
+    uint32_t carry_err = 0;
+    if (c.widx > 0) {
+      uint32_t mp = ~__byte_perm(c.prev, 0, 0x0123);
+      if (mp == 0) {
+        start = -32;
+        carry_err = GC_DEV_BAD_LD;  // a run of >= 32 ones
+      } else {
+        start = -(int32_t)(__ffs(mp) - 1);  // one bit after the previous word's last 0
+      }
+    }
+    uint32_t m = ~s;
+    uint32_t q = 0;
+    while (m) {
+      int32_t z = (int32_t)__clz(m);
+      uint32_t u = (uint32_t)(z - start + 1);  // LD = code length in bits
+      Grp g = grp0();
+      g.q0 = q;
+      g.nq = 1;
+      g.d0 = CG * start;
+      g.err = (u > 32u / CG) ? GC_DEV_BAD_LD : carry_err;
+      g.bw = g.err ? 32u : CG * u;  // BW = CG*LD
+      g.dlen = g.bw;
+      f(g);
+      carry_err = 0;
+      q++;
+      start = z + 1;
+      m &= ~(0x80000000u >> z);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- Group-Scheme, incomplete unary
+// Codes never cross a byte; the rest of a byte after its last code is 1s (P:L312,
+// A17), i.e. the byte's low-order bits in MSB-first order.
+template <int CG>
+struct CodecGscIU {
+  static constexpr bool kExc = false;
+  static constexpr bool kNeedsPrev = false;
+  static constexpr bool kMultiQuad = false;
+  static constexpr bool kVectorGroups = false;
+  __device__ static WAgg agg(const WCtx& c) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t m = ~(c.w >> (8 * i)) & 0xFFu;
+      d += m ? CG * (9u - (uint32_t)__ffs(m)) : 0u;  // used bits = 8 - trailing ones
+    }
+    return WAgg{(uint32_t)__popc(~c.w), d, 0u};
+  }
+  template <class F>
+  __device__ static void walk(const WCtx& c, F&& f) {
+    int32_t dpos = 0;
+    uint32_t q = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t m = ~(c.w >> (8 * i)) & 0xFFu;
+      if (m == 0) {  // 0xFF: a byte with no code
+        Grp g = grp0();
+        g.q0 = q;
+        g.nq = 0;
+        g.d0 = dpos;
+        g.err = GC_DEV_BAD_LD;
+        f(g);
+        continue;
+      }
+      uint32_t mm = m << 24;
+      int32_t start = 0;
+      while (mm) {
+        int32_t z = (int32_t)__clz(mm);
+        uint32_t u = (uint32_t)(z - start + 1);
+        Grp g = grp0();
+        g.q0 = q;
+        g.nq = 1;
+        g.d0 = dpos + CG * start;
+        g.err = (u > 32u / CG) ? GC_DEV_BAD_LD : 0u;
+        g.bw = g.err ? 32u : CG * u;
+        g.dlen = g.bw;
+        f(g);
+        q++;
+        start = z + 1;
+        mm &= ~(0x80000000u >> z);
+      }
+      dpos += CG * start;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- Group-AFOR
+// Header byte (A22): bits 0-1 length code (8/16/32 quads), bits 2-6 bw-1, bit 7 = 0.
+// Each frame starts a fresh 128-bit vector: ceil(L*bw/32) vectors.
+struct CodecAFOR {
+  static constexpr bool kExc = false;
+  static constexpr bool kNeedsPrev = false;
+  static constexpr bool kMultiQuad = true;
+  static constexpr bool kVectorGroups = true;
+  __device__ static WAgg agg(const WCtx& c) {
+    uint32_t q = 0, d = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t h = (c.w >> (8 * i)) & 0xFFu;
+      uint32_t L = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
+      uint32_t bw = ((h >> 2) & 31u) + 1u;
+      q += L;
+      d += 32u * ((L * bw + 31u) / 32u);
+    }
+    return WAgg{q, d, 0u};
+  }
+  template <class F>
+  __device__ static void walk(const WCtx& c, F&& f) {
+    uint32_t q = 0;
+    int32_t d = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t h = (c.w >> (8 * i)) & 0xFFu;
+      Grp g = grp0();
+      g.q0 = q;
+      g.nq = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
+      g.bw = ((h >> 2) & 31u) + 1u;
+      g.step = g.bw;
+      g.d0 = d;
+      g.dlen = 32u * ((g.nq * g.bw + 31u) / 32u);
+      g.err = ((h & 3u) == 3u || (h & 0x80u)) ? GC_DEV_BAD_FRAME : 0u;
+      f(g);
+      q += g.nq;
+      d += (int32_t)g.dlen;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- Group-PFD
+// Batch-form frame header (A31): byte 0 = b, byte 1 = wcode (0 none, 1/2/3 -> 8/16/32-bit
+// values), bytes 2-3 = exception count (LE).  Exceptions of the frame live in the
+// exception stream: count positions (u8, or u16 LE when 4F > 256) then count values.
+template <int F>
+struct CodecPFD {
+  static constexpr bool kExc = true;
+  static constexpr bool kNeedsPrev = false;
+  static constexpr bool kMultiQuad = true;
+  static constexpr bool kVectorGroups = true;
+  static constexpr uint32_t kPosBytes = 4 * F <= 256 ? 1u : 2u;
+  __device__ static __forceinline__ uint32_t frame_q(const WCtx& c) {
+    uint64_t first = c.widx * (uint64_t)F;
+    return c.Q > first ? (uint32_t)mn64((uint64_t)F, c.Q - first) : 0u;
+  }
+  __device__ static __forceinline__ void decode_hdr(const WCtx& c, Grp& g) {
+    uint32_t b = c.w & 0xFFu, wc = (c.w >> 8) & 0xFFu, cnt = c.w >> 16;
+    uint32_t q = frame_q(c);
+    g.err = 0;
+    if (b < 1 || b > 32 || wc > 3) g.err |= GC_DEV_BAD_FRAME;
+    if (cnt > 4 * q || (cnt > 0 && wc == 0)) g.err |= GC_DEV_BAD_EXCEPTION;
+    g.bw = (b >= 1 && b <= 32) ? b : 32u;
+    g.step = g.bw;
+    g.nq = F;
+    g.dlen = 32u * ((q * g.bw + 31u) / 32u);
+    g.wb = wc == 1 ? 1u : (wc == 2 ? 2u : (wc == 3 ? 4u : 0u));
+    g.cnt = g.err ? 0u : cnt;
+    g.elen = cnt * (kPosBytes + g.wb);
+  }
+  __device__ static WAgg agg(const WCtx& c) {
+    Grp g = grp0();
+    decode_hdr(c, g);
+    return WAgg{(uint32_t)F, g.dlen, g.elen};
+  }
+  template <class F2>
+  __device__ static void walk(const WCtx& c, F2&& f) {
+    Grp g = grp0();
+    decode_hdr(c, g);
+    f(g);
+  }
+};
+
+}  // namespace gcd

@@ -1,0 +1,965 @@
+// gc_kernels.cu -- the B200 (sm_100a) decode path and the C ABI of include/gc.h.
+//
+// Hot path of gc_decode_dgaps:
+//   1. k_index  (subsystem (a)): control-space tiles of 2048
+//      words parse every control word, run a device-wide segmented exclusive scan
+//      (block scan + decoupled look-back, segmented by list) of (quads, data
+//      lane-bits, exception bytes), and write one Entry per output tile: where the
+//      quad containing output position t*kT starts in the control, data and
+//      exception streams.
+//   2. k_decode (subsystems (b)-(d), a3-a6): output-space tiles of 4096 ints.  A
+//      tile stages its control words, data vectors and exceptions into shared
+//      memory with 1-D bulk async copies (TMA engine), re-parses its control words
+//      from the Entry (block scans), expands groups into per-quad descriptors,
+//      unpacks one quad per thread-slot with shift/mask over the four vertical
+//      lanes (the paper's high-first split for values that cross a word), patches
+//      Group-PFD exceptions in shared memory, runs the segmented d-gap inclusive
+//      scan (thread-serial + block + decoupled look-back across tiles) and writes
+//      the tile with coalesced 128-bit stores.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "gc.h"
+#include "gc_codecs.cuh"
+#include "gc_device.cuh"
+
+namespace gcd {
+
+struct Dev {
+  uint64_t n_lists;
+  const uint32_t* list_n;
+  const uint64_t* ctrl_off;
+  const uint64_t* data_off;
+  const uint64_t* exc_off;
+  const uint64_t* out_off;
+  const uint32_t* ctrl_words;
+  uint64_t n_ctrl_words;
+  const uint4* data;
+  uint64_t data_vectors;
+  const uint8_t* exc;
+  uint64_t exc_bytes;
+  uint64_t total_out;
+  uint32_t n_tiles_a, n_tiles_b;
+  WsHeader* hdr;
+  TileA* tiles_a;
+  uint64_t* tiles_b;
+  Entry* entries;
+};
+
+// Per-thread cursor over the lists of consecutive control words.
+struct ListCur {
+  uint64_t l;        // list index (n_lists = past the end)
+  uint64_t cw_lo;    // first control word of the list
+  uint64_t cw_hi;    // one past its last control word
+  uint64_t n, Q;     // ints, quads
+  uint64_t oo;       // out_off
+  uint64_t dbase;    // data_off * 32 (lane bits)
+  uint64_t ebase;    // exc_off
+  uint64_t dlim, elim;  // data_off[l+1]*32, exc_off[l+1]
+  __device__ void load(const Dev& D, uint64_t li) {
+    l = li;
+    if (li >= D.n_lists) {
+      cw_lo = cw_hi = ~0ull;
+      n = Q = 0;
+      return;
+    }
+    cw_lo = D.ctrl_off[li] >> 2;
+    cw_hi = D.ctrl_off[li + 1] >> 2;
+    n = D.list_n[li];
+    Q = (n + 3) >> 2;
+    oo = D.out_off[li];
+    dbase = D.data_off[li] * 32ull;
+    dlim = D.data_off[li + 1] * 32ull;
+    ebase = D.exc_off ? D.exc_off[li] : 0ull;
+    elim = D.exc_off ? D.exc_off[li + 1] : 0ull;
+  }
+  // advance to the list owning control word w (skips lists without control words)
+  __device__ void seek(const Dev& D, uint64_t w) {
+    if (l < D.n_lists && w < cw_hi) return;
+    uint64_t li = l;
+    while (li < D.n_lists && (D.ctrl_off[li + 1] >> 2) <= w) li++;
+    load(D, li);
+  }
+};
+
+// Largest l in [lo, hi) with ctrl_off[l] <= key (assumes ctrl_off[lo] <= key).
+__device__ __forceinline__ uint64_t find_list(const uint64_t* off, uint64_t lo, uint64_t hi,
+                                              uint64_t key) {
+  uint64_t a = lo, b = hi;
+  while (b - a > 1) {
+    uint64_t m = (a + b) >> 1;
+    if (off[m] <= key)
+      a = m;
+    else
+      b = m;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void report(uint32_t* s_err, uint32_t bits) {
+  if (bits) atomicOr(s_err, bits);
+}
+
+// =====================================================================================
+// k_validate: directory consistency (one pass over the lists, folded into the index
+// grid).  out_off must be the exclusive scan of list_n, offsets monotone and inside the
+// streams, every non-empty list must own at least one control word.
+// =====================================================================================
+__device__ void validate_lists(const Dev& D, uint32_t tile, uint32_t* s_err) {
+  uint64_t per = (D.n_lists + D.n_tiles_a - 1) / D.n_tiles_a;
+  uint64_t l0 = (uint64_t)tile * per, l1 = mn64(D.n_lists, l0 + per);
+  uint32_t err = 0;
+  for (uint64_t l = l0 + threadIdx.x; l < l1; l += kThreads) {
+    uint64_t n = D.list_n[l];
+    uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1];
+    uint64_t d0 = D.data_off[l], d1 = D.data_off[l + 1];
+    uint64_t o0 = D.out_off[l], o1 = D.out_off[l + 1];
+    bool bad = (o1 != o0 + n) || (c1 < c0) || (d1 < d0) || ((c0 | c1) & 3) ||
+               (c1 > 4 * D.n_ctrl_words) || (d1 > D.data_vectors) || (o1 > D.total_out) ||
+               (n > 0 && c1 == c0);
+    if (D.exc_off) {
+      uint64_t e0 = D.exc_off[l], e1 = D.exc_off[l + 1];
+      bad = bad || (e1 < e0) || (e1 > D.exc_bytes);
+    }
+    if (l == 0) bad = bad || (o0 != 0) || (c0 != 0);
+    if (l + 1 == D.n_lists) bad = bad || (o1 != D.total_out);
+    if (bad) err |= GC_DEV_TRUNCATED;
+  }
+  report(s_err, err);
+}
+
+// =====================================================================================
+// k_index (subsystem (a)): device-wide segmented scan over the control stream.
+// =====================================================================================
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_index(Dev D) {
+  __shared__ uint32_t s_w[kWA + 1];  // [0] = halo word (tile start - 1)
+  __shared__ Seg3 s_scr[kWarps];
+  __shared__ Seg3 s_prefix;
+  __shared__ uint32_t s_tile, s_err, s_first_reset;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_tile = atomicAdd(&D.hdr->counter_a, 1u);
+    s_err = 0;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  validate_lists(D, tile, &s_err);
+  const uint64_t w0 = (uint64_t)tile * kWA;
+  const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
+  for (uint32_t i = tid; i <= nw; i += kThreads) {
+    int64_t gw = (int64_t)w0 - 1 + (int64_t)i;
+    s_w[i] = (gw >= 0 && (uint64_t)gw < D.n_ctrl_words) ? D.ctrl_words[gw] : 0u;
+  }
+  __syncthreads();
+
+  const uint64_t my0 = w0 + (uint64_t)tid * kCA;
+  const uint32_t myn = my0 < w0 + nw ? (uint32_t)mn64(kCA, w0 + nw - my0) : 0u;
+  ListCur L;
+  L.load(D, myn ? find_list(D.ctrl_off, 0, D.n_lists + 1, 4 * my0) : D.n_lists);
+  const ListCur L0 = L;
+
+  // pass 1: per-word aggregates, segmented at list starts
+  Seg3 agg{0, 0, 0, 0};
+  for (uint32_t k = 0; k < myn; k++) {
+    uint64_t w = my0 + k;
+    L.seek(D, w);
+    if (L.l >= D.n_lists) break;
+    WCtx c;
+    c.w = s_w[w - w0 + 1];
+    c.prev = s_w[w - w0];
+    c.widx = w - L.cw_lo;
+    c.Q = L.Q;
+    WAgg a = C::agg(c);
+    Seg3 v = c.widx == 0 ? Seg3{1u, a.q, L.dbase + a.d, L.ebase + a.e} : Seg3{0u, a.q, a.d, a.e};
+    agg = seg3_op(agg, v);
+  }
+  if (tid == 0) s_first_reset = (myn && L0.l < D.n_lists && my0 == L0.cw_lo) ? 1u : 0u;
+  Seg3 total;
+  Seg3 excl = block_excl_seg3(agg, s_scr, &total);
+
+  // decoupled look-back across control tiles (thread 0)
+  if (tid == 0) {
+    TileA* me = D.tiles_a + tile;
+    if (total.f) {
+      me->iq = total.q;
+      me->id = total.d;
+      me->ie = total.e;
+      fence_gpu();
+      st_relaxed_u32(&me->flag, kFlagIncl);
+    } else {
+      me->aq = total.q;
+      me->ad = total.d;
+      me->ae = total.e;
+      fence_gpu();
+      st_relaxed_u32(&me->flag, kFlagAgg);
+    }
+    Seg3 pre{0, 0, 0, 0};
+    if (!s_first_reset) {
+      int64_t p = (int64_t)tile - 1;
+      while (p >= 0) {
+        TileA* t = D.tiles_a + p;
+        uint32_t f;
+        do {
+          f = ld_relaxed_u32(&t->flag);
+        } while (f == 0);
+        fence_gpu();
+        if (f == kFlagIncl) {
+          Seg3 v{1u, ld_relaxed_u32(&t->iq), ld_relaxed_u64(&t->id), ld_relaxed_u64(&t->ie)};
+          pre = seg3_op(v, pre);
+          break;
+        }
+        Seg3 v{0u, ld_relaxed_u32(&t->aq), ld_relaxed_u64(&t->ad), ld_relaxed_u64(&t->ae)};
+        pre = seg3_op(v, pre);
+        p--;
+      }
+      if (!total.f) {
+        Seg3 inc = seg3_op(pre, total);
+        me->iq = inc.q;
+        me->id = inc.d;
+        me->ie = inc.e;
+        fence_gpu();
+        st_relaxed_u32(&me->flag, kFlagIncl);
+      }
+    }
+    s_prefix = pre;
+  }
+  __syncthreads();
+
+  // pass 2: walk the groups with their prefixes; write tile Entries; check bounds
+  Seg3 S = seg3_op(s_prefix, excl);
+  L = L0;
+  uint32_t err = 0;
+  for (uint32_t k = 0; k < myn; k++) {
+    uint64_t w = my0 + k;
+    L.seek(D, w);
+    if (L.l >= D.n_lists) break;
+    WCtx c;
+    c.w = s_w[w - w0 + 1];
+    c.prev = s_w[w - w0];
+    c.widx = w - L.cw_lo;
+    c.Q = L.Q;
+    if (c.widx == 0) S = Seg3{1u, 0u, L.dbase, L.ebase};
+    const Seg3 SW = S;
+    C::walk(c, [&](const Grp& g) {
+      uint64_t gq = (uint64_t)SW.q + g.q0;
+      if (gq < L.Q && g.err) err |= g.err;
+      if (gq >= L.Q || g.nq == 0) return;
+      uint64_t ge = mn64(gq + g.nq, L.Q);
+      uint64_t gdata = SW.d + (int64_t)g.d0;
+      uint64_t gexc = SW.e + g.e0;
+      if (gdata < L.dbase || gdata + g.dlen > L.dlim) err |= GC_DEV_TRUNCATED;
+      if (C::kExc && gexc + g.elen > L.elim) err |= GC_DEV_TRUNCATED;
+      uint64_t lo_int = L.oo + 4 * gq;
+      uint64_t hi_int = L.oo + mn64(4 * ge, L.n);
+      uint64_t t = (lo_int + kT - 1) / kT;
+      if (t * kT < hi_int && t < D.n_tiles_b) {
+        uint64_t j = (t * kT - L.oo) >> 2;
+        Entry e;
+        e.l = (uint32_t)L.l;
+        e.j = (uint32_t)j;
+        e.wq = SW.q;
+        e.valid = 1;
+        e.gword = w;
+        e.wd = SW.d;
+        e.we = SW.e;
+        e.dbeg = gdata;
+        e.ebeg = gexc;
+        e.cend = w + 1;
+        if (j > gq) {  // the boundary splits a multi-quad group
+          e.dend = gdata + 32ull * (((j - gq) * g.step + 31) / 32);
+          e.eend = gexc + g.elen;
+        } else {
+          e.dend = gdata;
+          e.eend = gexc;
+        }
+        D.entries[t] = e;
+      }
+    });
+    WAgg a = C::agg(c);
+    S.q += a.q;
+    S.d += a.d;
+    S.e += a.e;
+    if (w + 1 == L.cw_hi && (uint64_t)S.q < L.Q) err |= GC_DEV_TRUNCATED;  // list not covered
+  }
+  report(&s_err, err);
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
+}
+
+// =====================================================================================
+// k_decode (subsystems (b)-(d)): one output tile of kT ints per CTA.
+// =====================================================================================
+struct DecodeSmem {
+  static constexpr uint32_t kOutOff = 0;
+  static constexpr uint32_t kDescOff = kOutOff + kOutChunks * 16;
+  static constexpr uint32_t kDataOff = kDescOff + kRQ * 8;
+  static constexpr uint32_t kCtrlOff = kDataOff + kDCap * 16;
+  static constexpr uint32_t kExcOff = kCtrlOff + kCCap * 4;
+  static constexpr uint32_t kResetOff0 = kExcOff;
+  __host__ __device__ static constexpr uint32_t reset_off(bool exc) { return kExcOff + (exc ? kECap : 0); }
+  __host__ __device__ static constexpr uint32_t bytes(bool exc) { return reset_off(exc) + kResetWords * 4; }
+};
+
+template <class C, bool DGAPS>
+__global__ void __launch_bounds__(kThreads, 4) k_decode(Dev D, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint4* s_out4 = reinterpret_cast<uint4*>(smem + DecodeSmem::kOutOff);
+  uint32_t* s_out = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kOutOff);
+  uint2* s_desc = reinterpret_cast<uint2*>(smem + DecodeSmem::kDescOff);
+  uint4* s_data = reinterpret_cast<uint4*>(smem + DecodeSmem::kDataOff);
+  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kCtrlOff);
+  uint32_t* s_reset = reinterpret_cast<uint32_t*>(smem + DecodeSmem::reset_off(C::kExc));
+  uint8_t* s_exc = smem + DecodeSmem::kExcOff;
+
+  __shared__ Entry s_e0, s_e1;
+  __shared__ Seg3 s_scr3[kWarps];
+  __shared__ uint32_t s_scr1[kWarps];
+  __shared__ Seg1 s_scrs[kWarps];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint32_t s_tile, s_err, s_carry;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_tile = atomicAdd(&D.hdr->counter_b, 1u);
+    s_err = 0;
+    s_carry = 0;
+    const uint32_t t = s_tile;
+    s_e0 = D.entries[t];
+    if (t + 1 < D.n_tiles_b) {
+      s_e1 = D.entries[t + 1];
+    } else {
+      Entry e;
+      memset(&e, 0, sizeof(e));
+      e.l = (uint32_t)D.n_lists;
+      e.valid = 1;
+      e.cend = D.ctrl_off[D.n_lists] >> 2;
+      e.dend = D.data_off[D.n_lists] * 32ull;
+      e.eend = D.exc_off ? D.exc_off[D.n_lists] : 0ull;
+      s_e1 = e;
+    }
+    mbar_init(&s_bar, 1);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const Entry E0 = s_e0, E1 = s_e1;
+  const int64_t base_int = (int64_t)tile * kT - 4;  // global int at staging index 0
+
+  if (!E0.valid || !E1.valid || E1.cend <= E0.gword || E0.l >= D.n_lists) {
+    if (tid == 0) {
+      atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
+      if (DGAPS) st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
+    }
+    return;
+  }
+
+  // ---- ranges of the three streams this tile needs
+  const uint64_t wa = E0.gword, wb = E1.cend;
+  const uint64_t cbase = (wa ? wa - 1 : 0) & ~3ull;
+  const uint64_t cstop = mn64((wb + 3) & ~3ull, D.n_ctrl_words);
+  const bool ctrl_staged = cstop - cbase <= kCCap;
+  const uint64_t va = E0.dbeg >> 5;
+  const uint64_t vb = mx64(va, mn64((E1.dend + 31) >> 5, D.data_vectors));
+  const bool data_staged = vb - va <= kDCap;
+  uint64_t ea = 0, eb = 0;
+  bool exc_staged = false;
+  if (C::kExc) {
+    ea = E0.ebeg & ~15ull;
+    eb = mx64(ea, mn64((E1.eend + 15) & ~15ull, D.exc_bytes));
+    exc_staged = eb - ea <= kECap;
+  }
+  if (tid == 0) {
+    uint32_t bytes = 0;
+    if (ctrl_staged && cstop > cbase) bytes += (uint32_t)(cstop - cbase) * 4;
+    if (data_staged && vb > va) bytes += (uint32_t)(vb - va) * 16;
+    if (C::kExc && exc_staged && eb > ea) bytes += (uint32_t)(eb - ea);
+    mbar_expect_tx(&s_bar, bytes);
+    if (ctrl_staged && cstop > cbase)
+      bulk_g2s(s_ctrl, D.ctrl_words + cbase, (uint32_t)(cstop - cbase) * 4, &s_bar);
+    if (data_staged && vb > va) bulk_g2s(s_data, D.data + va, (uint32_t)(vb - va) * 16, &s_bar);
+    if (C::kExc && exc_staged && eb > ea) bulk_g2s(s_exc, D.exc + ea, (uint32_t)(eb - ea), &s_bar);
+  }
+  const uint4* dptr = data_staged ? s_data : D.data + va;
+  const uint64_t dlim = vb - va;
+
+  // ---- output window of this tile
+  int64_t out_lo = (int64_t)(D.out_off[E0.l] + 4ull * E0.j);
+  int64_t out_hi = E1.l < D.n_lists ? (int64_t)(D.out_off[E1.l] + 4ull * E1.j) : (int64_t)D.total_out;
+  {
+    int64_t clo = smax64(base_int, 0), chi = smin64(base_int + kOutWords, (int64_t)D.total_out);
+    if (out_lo < clo || out_hi > chi || out_hi < out_lo) {
+      if (tid == 0) atomicOr(&s_err, (uint32_t)GC_DEV_TRUNCATED);
+      out_lo = smax64(out_lo, clo);
+      out_hi = smax64(out_lo, smin64(out_hi, chi));
+    }
+  }
+  const uint32_t lo_loc = (uint32_t)(out_lo - base_int), hi_loc = (uint32_t)(out_hi - base_int);
+  for (uint32_t i = tid; i < kResetWords; i += kThreads) s_reset[i] = 0;
+  for (uint32_t i = tid; i < lo_loc + (kOutWords - hi_loc); i += kThreads)
+    s_out[sw_word(i < lo_loc ? i : hi_loc + (i - lo_loc))] = 0;
+
+  mbar_wait(&s_bar, 0);
+  __syncthreads();
+
+  auto cword = [&](uint64_t w) -> uint32_t {
+    if (ctrl_staged) return (w >= cbase && w < cstop) ? s_ctrl[w - cbase] : 0u;
+    return w < D.n_ctrl_words ? D.ctrl_words[w] : 0u;
+  };
+  auto excb = [&](uint64_t b) -> uint32_t {
+    if (exc_staged) return (b >= ea && b < eb) ? s_exc[b - ea] : 0u;
+    return b < D.exc_bytes ? D.exc[b] : 0u;
+  };
+
+  uint32_t err = 0;
+  Seg3 carry{1u, E0.wq, E0.wd, E0.we};  // state at the start of word wa
+  const uint64_t lend = mn64((uint64_t)E1.l + 1, D.n_lists);
+
+  for (uint64_t r0 = wa; r0 < wb; r0 += kRoundWords) {
+    const uint64_t my0 = r0 + (uint64_t)tid * kCB;
+    const uint32_t myn = my0 < wb ? (uint32_t)mn64(kCB, wb - my0) : 0u;
+    ListCur L0;
+    L0.load(D, myn ? find_list(D.ctrl_off, E0.l, lend, 4 * my0) : D.n_lists);
+
+    // generic walk over my words: f(L, SW, c, g) per group; returns nothing
+    auto for_groups = [&](Seg3 S, auto&& f) {
+      ListCur L = L0;
+      for (uint32_t k = 0; k < myn; k++) {
+        uint64_t w = my0 + k;
+        L.seek(D, w);
+        if (L.l >= D.n_lists) break;
+        WCtx c;
+        c.w = cword(w);
+        c.prev = C::kNeedsPrev ? cword(w - 1) : 0u;
+        c.widx = w - L.cw_lo;
+        c.Q = L.Q;
+        if (c.widx == 0 && w != wa) S = Seg3{1u, 0u, L.dbase, L.ebase};
+        const Seg3 SW = S;
+        const uint64_t klo = L.l == E0.l ? E0.j : 0ull;
+        const uint64_t khi = mn64(L.Q, L.l == E1.l ? (uint64_t)E1.j : L.Q);
+        C::walk(c, [&](const Grp& g) {
+          uint64_t gq = (uint64_t)SW.q + g.q0;
+          uint64_t ka = mx64(gq, klo), kb = mn64(gq + g.nq, khi);
+          if (ka < kb) f(L, SW, g, gq, ka, kb);
+        });
+        WAgg a = C::agg(c);
+        S.q += a.q;
+        S.d += a.d;
+        S.e += a.e;
+      }
+    };
+
+    // pass 1: aggregates -> segmented block scan with the carry
+    Seg3 agg{0, 0, 0, 0};
+    {
+      ListCur L = L0;
+      for (uint32_t k = 0; k < myn; k++) {
+        uint64_t w = my0 + k;
+        L.seek(D, w);
+        if (L.l >= D.n_lists) break;
+        WCtx c;
+        c.w = cword(w);
+        c.prev = C::kNeedsPrev ? cword(w - 1) : 0u;
+        c.widx = w - L.cw_lo;
+        c.Q = L.Q;
+        WAgg a = C::agg(c);
+        Seg3 v = (c.widx == 0 && w != wa) ? Seg3{1u, a.q, L.dbase + a.d, L.ebase + a.e}
+                                          : Seg3{0u, a.q, a.d, a.e};
+        agg = seg3_op(agg, v);
+      }
+    }
+    Seg3 total;
+    Seg3 excl = block_excl_seg3(agg, s_scr3, &total);
+    const Seg3 S0 = seg3_op(carry, excl);
+    carry = seg3_op(carry, total);
+
+    // pass 2: kept quads -> local quad indices
+    uint32_t kept = 0;
+    for_groups(S0, [&](const ListCur&, const Seg3&, const Grp&, uint64_t, uint64_t ka,
+                       uint64_t kb) { kept += (uint32_t)(kb - ka); });
+    uint32_t K;
+    const uint32_t lq0 = block_excl_sum(kept, s_scr1, &K);
+
+    for (uint32_t u = 0; u < K; u += kRQ) {
+      // pass 3: descriptors of the quads [u, u+kRQ)
+      uint32_t x = lq0;
+      for_groups(S0, [&](const ListCur& L, const Seg3& SW, const Grp& g, uint64_t gq,
+                         uint64_t ka, uint64_t kb) {
+        uint32_t cnt = (uint32_t)(kb - ka);
+        if (x + cnt > u && x < u + kRQ) {
+          int64_t gbit = (int64_t)(SW.d + (int64_t)g.d0) - (int64_t)(va * 32);
+          for (uint64_t j = ka; j < kb; j++, x++) {
+            if (x < u || x >= u + kRQ) continue;
+            int64_t pos = gbit + (int64_t)((j - gq) * g.step);
+            int64_t op = (int64_t)(L.oo + 4 * j) - base_int;
+            uint32_t c = (uint32_t)mn64(4, L.n - 4 * j);
+            bool ok = pos >= 0 && op >= (int64_t)lo_loc && op + c <= (int64_t)hi_loc;
+            if (!ok) err |= GC_DEV_TRUNCATED;
+            s_desc[x - u] = make_uint2(ok ? (uint32_t)pos : 0xFFFFFFFFu,
+                                       g.bw | ((uint32_t)op << 6) | ((c - 1) << 19));
+            if (DGAPS && j == 0 && ok) atomicOr(&s_reset[op >> 5], 1u << (op & 31));
+          }
+        } else {
+          x += cnt;
+        }
+      });
+      __syncthreads();
+      // unpack: 4 consecutive quads per thread (thread-per-quad on the 4 vertical lanes)
+      const uint32_t nr = mn32(kRQ, K - u);
+#pragma unroll
+      for (int s = 0; s < 4; s++) {
+        uint32_t qi = 4 * tid + s;
+        if (qi >= nr) break;
+        uint2 d = s_desc[qi];
+        if (d.x == 0xFFFFFFFFu) continue;
+        uint32_t bw = d.y & 63u, op = (d.y >> 6) & 0x1FFFu, c = ((d.y >> 19) & 3u) + 1u;
+        uint32_t m = d.x >> 5, off = d.x & 31u;
+        bool straddle = off + bw > 32;
+        if (m >= dlim || (straddle && m + 1 >= dlim)) {
+          err |= GC_DEV_TRUNCATED;
+          continue;
+        }
+        uint4 v0 = dptr[m];
+        uint4 v1 = straddle ? dptr[m + 1] : make_uint4(0, 0, 0, 0);
+        uint32_t lo_len = straddle ? off + bw - 32 : 0u;
+        uint32_t mk = mask_bits(bw), ml = (1u << lo_len) - 1u;
+        // high part from the current vector, low part from the next (A3)
+        uint32_t x0 = (((v0.x >> off) << lo_len) | (v1.x & ml)) & mk;
+        uint32_t x1 = (((v0.y >> off) << lo_len) | (v1.y & ml)) & mk;
+        uint32_t x2 = (((v0.z >> off) << lo_len) | (v1.z & ml)) & mk;
+        uint32_t x3 = (((v0.w >> off) << lo_len) | (v1.w & ml)) & mk;
+        s_out[sw_word(op)] = x0;
+        if (c > 1) s_out[sw_word(op + 1)] = x1;
+        if (c > 2) s_out[sw_word(op + 2)] = x2;
+        if (c > 3) s_out[sw_word(op + 3)] = x3;
+      }
+      __syncthreads();
+    }
+
+    if (C::kExc) {
+      // Group-PFD step 3: write each exception into its slot, before the scan
+      for_groups(S0, [&](const ListCur& L, const Seg3& SW, const Grp& g, uint64_t gq,
+                         uint64_t ka, uint64_t kb) {
+        const uint32_t posb = (4 * g.nq <= 256) ? 1u : 2u;
+        const uint64_t e0 = SW.e + g.e0;
+        const uint32_t qf = (uint32_t)mn64(g.nq, L.Q - gq);
+        uint32_t prev = 0;
+        for (uint32_t i = 0; i < g.cnt; i++) {
+          uint32_t p = excb(e0 + (uint64_t)i * posb);
+          if (posb == 2) p |= excb(e0 + (uint64_t)i * posb + 1) << 8;
+          if (p >= 4 * qf || (i > 0 && p <= prev)) {
+            err |= GC_DEV_BAD_EXCEPTION;
+            break;
+          }
+          prev = p;
+          uint64_t j = gq + (p >> 2);
+          if (j < ka || j >= kb) continue;
+          uint64_t gi = 4 * j + (p & 3);
+          if (gi >= L.n) continue;
+          uint64_t vb0 = e0 + (uint64_t)g.cnt * posb + (uint64_t)i * g.wb;
+          uint32_t v = 0;
+          for (uint32_t t = 0; t < g.wb; t++) v |= excb(vb0 + t) << (8 * t);
+          int64_t op = (int64_t)(L.oo + gi) - base_int;
+          s_out[sw_word((uint32_t)op)] = v;
+        }
+      });
+      __syncthreads();
+    }
+  }
+
+  // ---- segmented d-gap inclusive scan: thread-serial, block, look-back
+  if (DGAPS) {
+    // thread i owns staging ints [4+16i, 20+16i); thread 0 also the head chunk [0,4)
+    const uint32_t c_first = tid == 0 ? 0u : 1u + 4u * tid;
+    const uint32_t nchunk = tid == 0 ? 5u : 4u;
+    uint32_t run = 0, fl = 0;
+    for (uint32_t s = 0; s < nchunk; s++) {
+      uint32_t c = c_first + s;
+      uint4 v = s_out4[sw_chunk(c)];
+      uint32_t rb = (s_reset[(4 * c) >> 5] >> ((4 * c) & 31)) & 15u;
+      uint32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (rb & (1u << k)) {
+          run = a[k];
+          fl = 1;
+        } else {
+          run += a[k];
+        }
+      }
+    }
+    Seg1 tot;
+    Seg1 ex = block_excl_seg1(Seg1{fl, run}, s_scrs, &tot);
+    if (tid < 32) {
+      // the first segment continues a list begun in an earlier tile iff E0.j > 0
+      const bool need_carry = E0.j > 0;
+      if (tid == 0)
+        st_relaxed_u64(D.tiles_b + tile,
+                       ((uint64_t)((tot.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) | tot.v);
+      uint32_t cin = 0;
+      if (need_carry) {
+        cin = lookback_u32(D.tiles_b, tile);
+        if (tid == 0 && !tot.f)
+          st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + tot.v));
+      }
+      if (tid == 0) s_carry = cin;
+    }
+    __syncthreads();
+    uint32_t add = ex.v + (ex.f ? 0u : s_carry);
+    bool seen = false;
+    run = 0;
+    for (uint32_t s = 0; s < nchunk; s++) {
+      uint32_t c = c_first + s;
+      uint4 v = s_out4[sw_chunk(c)];
+      uint32_t rb = (s_reset[(4 * c) >> 5] >> ((4 * c) & 31)) & 15u;
+      uint32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (rb & (1u << k)) {
+          run = a[k];
+          seen = true;
+        } else {
+          run += a[k];
+        }
+        a[k] = seen ? run : run + add;
+      }
+      s_out4[sw_chunk(c)] = make_uint4(a[0], a[1], a[2], a[3]);
+    }
+    __syncthreads();
+  }
+
+  // ---- coalesced 128-bit store of [out_lo, out_hi)
+  {
+    const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
+    const int64_t cb = base_int / 4;
+    for (int64_t c = c_lo + tid; c < c_hi; c += kThreads) {
+      uint4 v = s_out4[sw_chunk((uint32_t)(c - cb))];
+      int64_t g = 4 * c;
+      if (g >= out_lo && g + 4 <= out_hi) {
+        __stcs(reinterpret_cast<uint4*>(out + g), v);
+      } else {
+        uint32_t a[4] = {v.x, v.y, v.z, v.w};
+        for (int k = 0; k < 4; k++)
+          if (g + k >= out_lo && g + k < out_hi) out[g + k] = a[k];
+      }
+    }
+  }
+  report(&s_err, err);
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
+}
+
+// =====================================================================================
+// checksum (verification only, G7)
+// =====================================================================================
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_checksum(const uint32_t* __restrict__ list_n, const uint64_t* __restrict__ out_off,
+                           uint64_t n_lists, const uint32_t* __restrict__ out, uint64_t total,
+                           uint64_t list_base, unsigned long long* sums) {
+  const uint64_t per = 1024;
+  uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * per;
+  unsigned long long h = 0, s = 0, cnt = 0;
+  if (g0 < total) {
+    uint64_t l = find_list(out_off, 0, n_lists, g0);
+    while (l + 1 < n_lists && out_off[l + 1] <= g0) l++;
+    uint64_t g1 = mn64(total, g0 + per);
+    for (uint64_t g = g0; g < g1; g++) {
+      while (out_off[l + 1] <= g) l++;
+      uint64_t i = g - out_off[l];
+      uint64_t d = out[g];
+      h += mix64((((l + list_base) << 32) | i) ^ (d * 0x9E3779B97F4A7C15ull));
+      s += d;
+    }
+  }
+  for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_lists;
+       l += (uint64_t)gridDim.x * blockDim.x)
+    cnt += list_n[l];
+  for (int o = 16; o > 0; o >>= 1) {
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(sums + 0, h);
+    atomicAdd(sums + 1, s);
+    atomicAdd(sums + 2, cnt);
+  }
+}
+
+}  // namespace gcd
+
+// =====================================================================================
+// host side
+// =====================================================================================
+using namespace gcd;
+
+namespace {
+
+struct WsLayout {
+  uint64_t n_tiles_a, n_tiles_b;
+  uint64_t off_tiles_a, off_tiles_b, off_entries, bytes;
+};
+
+WsLayout ws_layout(const gc_batch* b) {
+  WsLayout L;
+  uint64_t words = b->ctrl_bytes / 4;
+  L.n_tiles_a = (words + kWA - 1) / kWA;
+  if (L.n_tiles_a == 0) L.n_tiles_a = 1;
+  L.n_tiles_b = (b->total_out + kT - 1) / kT;
+  L.off_tiles_a = sizeof(WsHeader);
+  L.off_tiles_b = L.off_tiles_a + L.n_tiles_a * sizeof(TileA);
+  L.off_entries = L.off_tiles_b + ((L.n_tiles_b * 8 + 255) & ~255ull);
+  L.bytes = L.off_entries + L.n_tiles_b * sizeof(Entry);
+  return L;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+gc_status check_codec(const gc_batch* b) {
+  switch (b->codec) {
+    case GC_GROUP_SIMPLE:
+    case GC_GROUP_AFOR:
+      return b->variant == 0 ? GC_OK : GC_ERR_BAD_VARIANT;
+    case GC_GROUP_SCHEME: {
+      uint32_t kind = (b->variant >> 2) & 3u, cg = 1u << (b->variant & 3u);
+      if (b->variant > 15 || kind > 2 || (kind == 2 && cg < 4)) return GC_ERR_BAD_VARIANT;
+      return GC_OK;
+    }
+    case GC_GROUP_PFD:
+      return (b->pfd_frame_quads == 32 || b->pfd_frame_quads == 128) ? GC_OK : GC_ERR_BAD_VARIANT;
+    default:
+      return GC_ERR_UNKNOWN_CODEC;
+  }
+}
+
+gc_status check_batch(const gc_batch* b, bool device_ptrs) {
+  if (!b) return GC_ERR_INVALID_ARGUMENT;
+  gc_status s = check_codec(b);
+  if (s != GC_OK) return s;
+  if (!b->list_n && b->n_lists) return GC_ERR_INVALID_ARGUMENT;
+  if (!b->ctrl_off || !b->data_off || !b->out_off) return GC_ERR_INVALID_ARGUMENT;
+  if (b->codec == GC_GROUP_PFD && !b->exc_off) return GC_ERR_INVALID_ARGUMENT;
+  if ((b->ctrl_bytes % 16) || (b->exc_bytes % 16)) return GC_ERR_INVALID_ARGUMENT;
+  if (b->ctrl_bytes && (!b->ctrl || !aligned16(b->ctrl))) return GC_ERR_INVALID_ARGUMENT;
+  if (b->data_vectors && (!b->data || !aligned16(b->data))) return GC_ERR_INVALID_ARGUMENT;
+  if (b->exc_bytes && (!b->exc || !aligned16(b->exc))) return GC_ERR_INVALID_ARGUMENT;
+  if (b->total_out && !b->n_lists) return GC_ERR_INVALID_ARGUMENT;
+  if (b->total_out > (1ull << 40) || b->n_lists > 0xFFFFFFF0ull) return GC_ERR_INVALID_ARGUMENT;
+  (void)device_ptrs;
+  return GC_OK;
+}
+
+gc_status check_device() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0;
+    cudaDeviceProp prop;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
+      return GC_ERR_CUDA;
+    ok = prop.major == 10 ? 1 : 0;
+  }
+  return ok ? GC_OK : GC_ERR_UNSUPPORTED_DEVICE;
+}
+
+template <class C>
+gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st) {
+  k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+  if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+  if (D.n_tiles_b == 0) return GC_OK;
+  const uint32_t smem = DecodeSmem::bytes(C::kExc);
+  static bool attr_set[2] = {false, false};
+  auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
+  if (!attr_set[dgaps]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return GC_ERR_CUDA;
+    attr_set[dgaps] = true;
+  }
+  kern<<<(unsigned)D.n_tiles_b, kThreads, smem, st>>>(D, out);
+  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
+gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                      void* stream, bool dgaps) {
+  gc_status s = check_batch(b, true);
+  if (s != GC_OK) return s;
+  if (!ws || !aligned16(ws) || (b->total_out && (!out || !aligned16(out))))
+    return GC_ERR_INVALID_ARGUMENT;
+  WsLayout L = ws_layout(b);
+  if (ws_bytes < L.bytes) return GC_ERR_WORKSPACE_TOO_SMALL;
+  s = check_device();
+  if (s != GC_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* w = (uint8_t*)ws;
+  if (cudaMemsetAsync(ws, 0, L.bytes, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (b->n_lists == 0 || b->total_out == 0) return GC_OK;
+  Dev D;
+  D.n_lists = b->n_lists;
+  D.list_n = b->list_n;
+  D.ctrl_off = b->ctrl_off;
+  D.data_off = b->data_off;
+  D.exc_off = b->codec == GC_GROUP_PFD ? b->exc_off : nullptr;
+  D.out_off = b->out_off;
+  D.ctrl_words = (const uint32_t*)b->ctrl;
+  D.n_ctrl_words = b->ctrl_bytes / 4;
+  D.data = (const uint4*)b->data;
+  D.data_vectors = b->data_vectors;
+  D.exc = b->exc;
+  D.exc_bytes = b->exc_bytes;
+  D.total_out = b->total_out;
+  D.n_tiles_a = (uint32_t)L.n_tiles_a;
+  D.n_tiles_b = (uint32_t)L.n_tiles_b;
+  D.hdr = (WsHeader*)w;
+  D.tiles_a = (TileA*)(w + L.off_tiles_a);
+  D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
+  D.entries = (Entry*)(w + L.off_entries);
+  switch (b->codec) {
+    case GC_GROUP_SIMPLE:
+      return launch_codec<CodecGS>(D, out, dgaps, st);
+    case GC_GROUP_AFOR:
+      return launch_codec<CodecAFOR>(D, out, dgaps, st);
+    case GC_GROUP_PFD:
+      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st)
+                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st);
+    default:
+      break;
+  }
+  switch (b->variant) {
+    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st);
+    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st);
+    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st);
+    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st);
+    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st);
+    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st);
+    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st);
+    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st);
+    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st);
+    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st);
+    default: return GC_ERR_BAD_VARIANT;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gc_abi_version(void) { return GC_ABI_VERSION; }
+
+const char* gc_status_string(gc_status s) {
+  switch (s) {
+    case GC_OK: return "ok";
+    case GC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case GC_ERR_UNKNOWN_CODEC: return "unknown codec";
+    case GC_ERR_BAD_VARIANT: return "bad variant";
+    case GC_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case GC_ERR_UNSUPPORTED_DEVICE: return "unsupported device (needs sm_100)";
+    case GC_ERR_CUDA: return "CUDA error";
+    case GC_ERR_NOT_INCREASING: return "list not strictly increasing";
+    case GC_ERR_NOMEM: return "out of host memory";
+  }
+  return "unknown status";
+}
+
+gc_status gc_workspace_size(const gc_batch* b, uint64_t* bytes) {
+  if (!b || !bytes) return GC_ERR_INVALID_ARGUMENT;
+  *bytes = ws_layout(b).bytes;
+  return GC_OK;
+}
+
+gc_status gc_decode(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes, void* stream) {
+  return decode_impl(b, out, ws, ws_bytes, stream, false);
+}
+
+gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          void* stream) {
+  return decode_impl(b, out, ws, ws_bytes, stream, true);
+}
+
+gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream) {
+  if (!ws || !host_bits) return GC_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(host_bits, ws, sizeof(uint32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
+gc_status gc_checksum(const gc_batch* b, const uint32_t* out, uint64_t list_base,
+                      uint64_t* dev_sum3, void* stream) {
+  if (!b || !dev_sum3 || (b->total_out && !out)) return GC_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(dev_sum3, 0, 24, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (b->n_lists == 0) return GC_OK;
+  uint64_t threads = (b->total_out + 1023) / 1024;
+  uint64_t blocks = (mx64(threads, b->n_lists / 64 + 1) + 255) / 256;
+  blocks = mn64(blocks, 1u << 20);
+  k_checksum<<<(unsigned)blocks, 256, 0, st>>>(b->list_n, b->out_off, b->n_lists, out,
+                                                 b->total_out, list_base,
+                                                 (unsigned long long*)dev_sum3);
+  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
+// --------------------------------------------------------------------------- host path
+static uint64_t al256(uint64_t x) { return (x + 255) & ~255ull; }
+
+gc_status gc_host_scratch_size(const gc_batch* hb, uint64_t* bytes) {
+  if (!hb || !bytes) return GC_ERR_INVALID_ARGUMENT;
+  uint64_t L = hb->n_lists;
+  uint64_t s = al256(4 * L) + 4 * al256(8 * (L + 1)) + al256(hb->ctrl_bytes) +
+               al256(16 * hb->data_vectors) + al256(hb->exc_bytes) + al256(4 * hb->total_out);
+  s += ws_layout(hb).bytes;
+  *bytes = s;
+  return GC_OK;
+}
+
+gc_status gc_decode_host(const gc_batch* hb, uint32_t* host_out, int dgaps, void* dev_scratch,
+                         uint64_t scratch_bytes, void* stream) {
+  gc_status s = check_batch(hb, false);
+  if (s != GC_OK) return s;
+  uint64_t need = 0;
+  gc_host_scratch_size(hb, &need);
+  if (!dev_scratch || ((uintptr_t)dev_scratch & 255u) || scratch_bytes < need ||
+      (hb->total_out && !host_out))
+    return GC_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* p = (uint8_t*)dev_scratch;
+  uint64_t L = hb->n_lists;
+  gc_batch d = *hb;
+  auto put = [&](const void* src, uint64_t bytes) -> void* {
+    void* dst = p;
+    p += al256(bytes);
+    if (bytes && cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return nullptr;
+    return dst;
+  };
+  d.list_n = (const uint32_t*)put(hb->list_n, 4 * L);
+  d.ctrl_off = (const uint64_t*)put(hb->ctrl_off, 8 * (L + 1));
+  d.data_off = (const uint64_t*)put(hb->data_off, 8 * (L + 1));
+  d.exc_off = nullptr;
+  if (hb->exc_off) d.exc_off = (const uint64_t*)put(hb->exc_off, 8 * (L + 1));
+  else p += al256(8 * (L + 1));
+  d.out_off = (const uint64_t*)put(hb->out_off, 8 * (L + 1));
+  d.ctrl = (const uint8_t*)put(hb->ctrl, hb->ctrl_bytes);
+  d.data = put(hb->data, 16 * hb->data_vectors);
+  d.exc = hb->exc_bytes ? (const uint8_t*)put(hb->exc, hb->exc_bytes) : nullptr;
+  if (!d.list_n || !d.ctrl_off || !d.data_off || !d.out_off || !d.ctrl || !d.data)
+    return GC_ERR_CUDA;
+  uint32_t* dout = (uint32_t*)p;
+  p += al256(4 * hb->total_out);
+  void* ws = p;
+  uint64_t wsb = ws_layout(hb).bytes;
+  s = decode_impl(&d, dout, ws, wsb, stream, dgaps != 0);
+  if (s != GC_OK) return s;
+  if (hb->total_out && cudaMemcpyAsync(host_out, dout, 4 * hb->total_out, cudaMemcpyDeviceToHost,
+                                       st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  return GC_OK;
+}
+
+}  // extern "C"

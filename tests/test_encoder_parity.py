@@ -1,0 +1,73 @@
+"""The product host encoder (libgc.so gc_encode_*) emits exactly the oracle's bytes,
+and the C-ABI library loads and exports every symbol include/gc.h declares (CPU only:
+no compute call needs a GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+from paper_1502_01916_b200 import gc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CODECS = ([(O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
+                                   for cg, k in gc.GSC_VARIANTS]
+          + [(O.GROUP_AFOR, 0), (O.GROUP_PFD, 0)])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_1502_01916_b200 import build
+    build.build()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "gc.h")).read()
+    declared = set(re.findall(r"\b(gc_[a-z_0-9]+)\s*\(", hdr))
+    lib = ctypes.CDLL(gc.LIB_PATH)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert declared and not missing, missing
+    assert gc.abi_version() == 1
+
+
+def _same(a: dict, b: gc.HostBatch):
+    for k in ("list_n", "ctrl_off", "data_off", "exc_off", "out_off"):
+        assert np.array_equal(np.asarray(a[k]), getattr(b, k)), k
+    assert np.array_equal(a["ctrl"], b.ctrl)
+    assert np.array_equal(a["data"].reshape(-1, 4), b.data)
+    assert np.array_equal(a["exc"], b.exc)
+
+
+@pytest.mark.parametrize("codec,variant", CODECS, ids=[gc.codec_label(c, v) for c, v in CODECS])
+def test_encoder_bytes_equal_oracle(codec, variant):
+    rng = np.random.default_rng(100 + 16 * codec + variant)
+    for max_len, bits, spike in ((9, 3, 0.0), (300, 12, 0.02), (2000, 20, 0.05), (70, 32, 0.0)):
+        w = gen.random_lists(rng, 60, max_len, bits, spike)
+        ref = O.encode_batch(w.values, w.list_n, codec, variant, threads=2)
+        got = gc.encode_batch(w.values, w.list_n, codec, variant, threads=3)
+        _same(ref, got)
+    w = gen.config(1, scale=1 / 32)
+    _same(O.encode_batch(w.values, w.list_n, codec, variant, delta=True),
+          gc.encode_batch(w.values, w.list_n, codec, variant, delta=True, threads=4))
+
+
+@pytest.mark.parametrize("zeta,F", [((3, 10), 32), ((1, 10), 128), ((1, 20), 32)])
+def test_encoder_pfd_parameters(zeta, F):
+    rng = np.random.default_rng(7)
+    w = gen.random_lists(rng, 40, 3000, 9, 0.08)
+    _same(O.encode_batch(w.values, w.list_n, O.GROUP_PFD, 0, frame_quads=F, zeta=zeta),
+          gc.encode_batch(w.values, w.list_n, O.GROUP_PFD, 0, frame_quads=F, zeta=zeta))
+
+
+def test_encoder_rejects_bad_input():
+    with pytest.raises(gc.GcError):
+        gc.encode_batch(np.array([5, 3], np.uint32), np.array([2], np.uint32), O.GROUP_SIMPLE,
+                        delta=True)
+    with pytest.raises(gc.GcError):
+        gc.encode_batch(np.array([1], np.uint32), np.array([1], np.uint32), O.GROUP_SCHEME,
+                        variant=gc.gsc_variant(1, "B") | (2 << 2))
+    with pytest.raises(gc.GcError):
+        gc.encode_batch(np.array([1], np.uint32), np.array([1], np.uint32), 9)

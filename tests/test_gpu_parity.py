@@ -1,0 +1,168 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the oracle and the
+generator, element by element.  Bar: bit-exact (integer work)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1502_01916_b200 import gc  # noqa: E402
+
+CODECS = ([(O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
+                                   for cg, k in gc.GSC_VARIANTS]
+          + [(O.GROUP_AFOR, 0), (O.GROUP_PFD, 0)])
+IDS = [gc.codec_label(c, v) for c, v in CODECS]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1502_01916_b200 import build
+    build.build()
+    torch.cuda.init()
+
+
+def gpu_decode(hb: gc.HostBatch, dgaps: bool):
+    db = gc.to_device(hb)
+    fn = gc.decode_dgaps if dgaps else gc.decode
+    out, ws = fn(db)
+    torch.cuda.synchronize()
+    status = gc.read_device_status(ws)
+    return out.cpu().numpy().view(np.uint32).copy(), status
+
+
+def check(values, list_n, codec, variant, frame_quads=32, zeta=(1, 10), delta=False,
+          encoder="oracle"):
+    if encoder == "oracle":
+        hb = gc.HostBatch.from_dict(O.encode_batch(values, list_n, codec, variant, delta=delta,
+                                                   frame_quads=frame_quads, zeta=zeta, threads=4))
+    else:
+        hb = gc.encode_batch(values, list_n, codec, variant, delta=delta, frame_quads=frame_quads,
+                             zeta=zeta)
+    gaps = O.decode_batch(hb.as_dict(), dgaps=False, threads=4)
+    docs = O.decode_batch(hb.as_dict(), dgaps=True, threads=4)
+    g, s1 = gpu_decode(hb, dgaps=False)
+    assert s1 == 0, gc.status_names(s1)
+    bad = np.nonzero(g != gaps)[0]
+    assert len(bad) == 0, f"gc_decode mismatch at {bad[:10]} ({len(bad)} total)"
+    d, s2 = gpu_decode(hb, dgaps=True)
+    assert s2 == 0, gc.status_names(s2)
+    bad = np.nonzero(d != docs)[0]
+    assert len(bad) == 0, f"gc_decode_dgaps mismatch at {bad[:10]} ({len(bad)} total)"
+    if delta:
+        assert np.array_equal(d, values)          # the generator's own docIDs
+    else:
+        assert np.array_equal(g, values)
+    return hb
+
+
+@pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
+def test_random_ragged(codec, variant):
+    rng = np.random.default_rng(1000 + 16 * codec + variant)
+    for n_lists, max_len, bits, spike in ((1, 5, 3, 0), (7, 40, 8, 0.0), (200, 3000, 14, 0.01),
+                                          (50, 20000, 22, 0.05), (30, 100, 32, 0.0)):
+        w = gen.random_lists(rng, n_lists, max_len, bits, spike)
+        check(w.values, w.list_n, codec, variant)
+
+
+@pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
+def test_edge_shapes(codec, variant):
+    """Empty lists, 1-int lists (thousands of lists per tile: control/data staging falls
+    back to global memory and tiles run several parse/unpack rounds), one list spanning
+    many tiles (look-back chains), lists ending exactly at tile boundaries, all-zero and
+    all-max values."""
+    rng = np.random.default_rng(7)
+    cases = []
+    ln = np.array([0, 0, 3, 0, 4096, 0, 1, 4095, 4097, 0], np.uint32)
+    cases.append((ln, rng.integers(0, 1 << 12, int(ln.sum())).astype(np.uint32)))
+    ln = np.ones(9000, np.uint32)
+    cases.append((ln, rng.integers(0, 1 << 32, 9000, dtype=np.uint64).astype(np.uint32)))
+    ln = rng.integers(1, 4, 6000).astype(np.uint32)
+    cases.append((ln, rng.integers(0, 1 << 9, int(ln.sum())).astype(np.uint32)))
+    ln = np.array([300_001], np.uint32)
+    cases.append((ln, rng.integers(0, 1 << 10, 300_001).astype(np.uint32)))
+    ln = np.array([5000, 70000], np.uint32)
+    cases.append((ln, np.zeros(75000, np.uint32)))
+    cases.append((ln, np.full(75000, 0xFFFFFFFF, np.uint32)))
+    for ln, v in cases:
+        check(v, ln, codec, variant)
+
+
+@pytest.mark.parametrize("F,zeta", [(32, (3, 10)), (128, (1, 10)), (32, (1, 50))])
+def test_pfd_parameters(F, zeta):
+    w = gen.config(3, scale=1 / 256)
+    check(w.values, w.list_n, O.GROUP_PFD, 0, frame_quads=F, zeta=zeta)
+
+
+@pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 1 / 64), (3, 1 / 64), (4, 1 / 256),
+                                     (5, 1 / 16384)])
+def test_configs_scaled_all_codecs(k, scale):
+    """The five BASELINE configs' shapes at reduced scale, every codec (docIDs pinned to the
+    generator for configs 1 and 5)."""
+    w = gen.config(k, scale=scale)
+    for codec, variant in CODECS:
+        check(w.values, w.list_n, codec, variant, delta=w.delta)
+
+
+def test_malformed_streams_flagged_not_faulting():
+    rng = np.random.default_rng(3)
+    w = gen.random_lists(rng, 20, 500, 10)
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SIMPLE))
+    hb.ctrl[0] = 0xFA                                         # selector 10
+    _, s = gpu_decode(hb, True)
+    assert s & 1
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_AFOR))
+    hb.ctrl[0] = 0x03                                         # length code 3
+    _, s = gpu_decode(hb, True)
+    assert s & 4
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_PFD))
+    hb.ctrl[0] = 0                                            # b = 0
+    _, s = gpu_decode(hb, True)
+    assert s & 4
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME,
+                                               O.gsc_variant(8, "CU")))
+    hb.ctrl[:8] = 0xFF                                        # runs of 32+ ones
+    _, s = gpu_decode(hb, True)
+    assert s & 2
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME,
+                                               O.gsc_variant(1, "B")))
+    hb.data_off = hb.data_off.copy()
+    hb.data_off[5:] = np.minimum(hb.data_off[5:], hb.data_off[5])  # truncated data
+    _, s = gpu_decode(hb, True)
+    assert s & 16
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME,
+                                               O.gsc_variant(2, "CU")))
+    hb.out_off = hb.out_off.copy()
+    hb.out_off[3] += 1                                        # inconsistent directory
+    _, s = gpu_decode(hb, True)
+    assert s & 16
+
+
+def test_host_path_and_checksum():
+    w = gen.config(1, scale=1 / 4)
+    hb = gc.encode_batch(w.values, w.list_n, O.GROUP_SCHEME, O.gsc_variant(4, "CU"), delta=True)
+    out = np.zeros(hb.total_out, np.uint32)
+    scratch = torch.empty(gc.host_scratch_size(hb), dtype=torch.uint8, device="cuda")
+    gc.decode_host(hb, out, True, scratch)
+    torch.cuda.synchronize()
+    assert np.array_equal(out, w.values)
+    db = gc.to_device(hb)
+    d, _ = gc.decode_dgaps(db)
+    sums = gc.checksum(db, d).cpu().numpy().view(np.uint64)
+    ref = gen.checksum(w.list_n, w.values)
+    assert [int(x) for x in sums] == list(ref)
+
+
+def test_api_errors():
+    w = gen.random_lists(np.random.default_rng(1), 3, 10, 4)
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SIMPLE))
+    db = gc.to_device(hb)
+    with pytest.raises(gc.GcError):
+        gc.decode(db, ws=torch.empty(16, dtype=torch.uint8, device="cuda"))
+    db.variant = 5
+    with pytest.raises(gc.GcError):
+        gc.decode(db)
