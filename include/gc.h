@@ -138,6 +138,17 @@ gc_status gc_decode(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_byte
 gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream);
 
+/* The same work as gc_decode (dgaps == 0) / gc_decode_dgaps (dgaps != 0) split into
+ * its three stream-ordered stages, for callers that time or overlap them:
+ *   GC_STAGE_RESET  zero the workspace (one cudaMemsetAsync),
+ *   GC_STAGE_INDEX  the control-stream scan kernel (subsystem (a)),
+ *   GC_STAGE_DECODE the fused unpack / patch / d-gap-scan / store kernel.
+ * stage_mask is any OR of the three; stages run in that order.  Calling the three
+ * stages one after another on one stream is exactly gc_decode / gc_decode_dgaps. */
+enum { GC_STAGE_RESET = 1, GC_STAGE_INDEX = 2, GC_STAGE_DECODE = 4, GC_STAGE_ALL = 7 };
+gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          void* stream, int dgaps, int stage_mask);
+
 /* Copy the sticky GC_DEV_* bits of a workspace to *host_bits.  Synchronises
  * `stream`.  0 means the last decode on this workspace saw a well-formed batch. */
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream);

@@ -769,10 +769,12 @@ gc_status check_device() {
 }
 
 template <class C>
-gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st) {
-  k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
-  if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-  if (D.n_tiles_b == 0) return GC_OK;
+gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
+  if (stages & GC_STAGE_INDEX) {
+    k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+  }
+  if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
   const uint32_t smem = DecodeSmem::bytes(C::kExc);
   static bool attr_set[2] = {false, false};
   auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
@@ -787,7 +789,7 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st)
 }
 
 gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
-                      void* stream, bool dgaps) {
+                      void* stream, bool dgaps, int stages = GC_STAGE_ALL) {
   gc_status s = check_batch(b, true);
   if (s != GC_OK) return s;
   if (!ws || !aligned16(ws) || (b->total_out && (!out || !aligned16(out))))
@@ -798,7 +800,8 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   if (s != GC_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* w = (uint8_t*)ws;
-  if (cudaMemsetAsync(ws, 0, L.bytes, st) != cudaSuccess) return GC_ERR_CUDA;
+  if ((stages & GC_STAGE_RESET) && cudaMemsetAsync(ws, 0, L.bytes, st) != cudaSuccess)
+    return GC_ERR_CUDA;
   if (b->n_lists == 0 || b->total_out == 0) return GC_OK;
   Dev D;
   D.n_lists = b->n_lists;
@@ -822,26 +825,26 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.entries = (Entry*)(w + L.off_entries);
   switch (b->codec) {
     case GC_GROUP_SIMPLE:
-      return launch_codec<CodecGS>(D, out, dgaps, st);
+      return launch_codec<CodecGS>(D, out, dgaps, st, stages);
     case GC_GROUP_AFOR:
-      return launch_codec<CodecAFOR>(D, out, dgaps, st);
+      return launch_codec<CodecAFOR>(D, out, dgaps, st, stages);
     case GC_GROUP_PFD:
-      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st)
-                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st);
+      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st, stages)
+                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st, stages);
     default:
       break;
   }
   switch (b->variant) {
-    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st);
-    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st);
-    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st);
-    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st);
-    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st);
-    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st);
-    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st);
-    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st);
-    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st);
-    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st);
+    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st, stages);
+    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st, stages);
+    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st, stages);
+    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st, stages);
+    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st, stages);
+    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st, stages);
+    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st, stages);
+    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st, stages);
+    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st, stages);
+    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st, stages);
     default: return GC_ERR_BAD_VARIANT;
   }
 }
@@ -880,6 +883,12 @@ gc_status gc_decode(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_byte
 gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream) {
   return decode_impl(b, out, ws, ws_bytes, stream, true);
+}
+
+gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          void* stream, int dgaps, int stage_mask) {
+  if (stage_mask & ~GC_STAGE_ALL) return GC_ERR_INVALID_ARGUMENT;
+  return decode_impl(b, out, ws, ws_bytes, stream, dgaps != 0, stage_mask);
 }
 
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream) {

@@ -59,6 +59,7 @@ def _lib():
             "gc_workspace_size": (i32, [P(CBatch), P(u64)]),
             "gc_decode": (i32, [P(CBatch), vp, vp, u64, vp]),
             "gc_decode_dgaps": (i32, [P(CBatch), vp, vp, u64, vp]),
+            "gc_decode_stage": (i32, [P(CBatch), vp, vp, u64, vp, i32, i32]),
             "gc_read_device_status": (i32, [vp, P(C.c_uint32), vp]),
             "gc_checksum": (i32, [P(CBatch), vp, u64, vp, vp]),
             "gc_host_scratch_size": (i32, [P(CBatch), P(u64)]),
@@ -274,6 +275,18 @@ def decode(batch: DeviceBatch, out=None, ws=None, stream=None):
 def decode_dgaps(batch: DeviceBatch, out=None, ws=None, stream=None):
     """gc_decode_dgaps: decode + per-list prefix sum mod 2^32 (docIDs)."""
     return _decode("gc_decode_dgaps", batch, out, ws, stream)
+
+
+STAGE_RESET, STAGE_INDEX, STAGE_DECODE, STAGE_ALL = 1, 2, 4, 7
+
+
+def decode_stage(batch: DeviceBatch, out, ws, dgaps: bool, stages: int, stream=None):
+    """gc_decode_stage: run a subset of the reset / index / decode stages."""
+    b = batch.cstruct()
+    st = _lib().gc_decode_stage(C.byref(b), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _stream_ptr(stream), int(dgaps), stages)
+    if st:
+        raise GcError(st, "gc_decode_stage")
 
 
 def read_device_status(ws, stream=None) -> int:
