@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""bench.py -- decoded uint32 ints/s of the Group-format decode + d-gap prefix-sum path
+on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+A step is one pass of the whole hot path (control scan, unpack, PFD patch, d-gap scan,
+store: gc_decode_dgaps) over one batch for every codec variant of the config.  The
+default workload is BASELINE.json configs[1]: Group-Scheme, all 10 granularity x
+length-descriptor variants, 2^26 ints in 10^5 lists.  Inputs are synthetic (gen/), encoded
+by the library's own host encoder, resident in HBM before timing; every working set
+(>= 380 MB per variant) is larger than the 126 MB L2.  Multi-GPU: one process per GPU
+(torchrun), lists sharded by rank (weak scaling: each rank decodes its own replica of the
+config), no collective on the data path; NCCL all-reduces counts and checksums after
+timing and the max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded uint32 ints/sec per codec (1/2/4/8 B200), % of HBM roofline"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--codecs", default="", help="comma list of labels (default: config's)")
+    ap.add_argument("--pfd-zeta", default="1/10")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+def config_codecs(k: int, zeta):
+    from paper_1502_01916_b200 import gc
+    if k == 1:
+        return [(gc.GROUP_SIMPLE, 0, 32, zeta)]
+    if k == 2:
+        return [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd), 32, zeta) for cg, kd in gc.GSC_VARIANTS]
+    if k == 3:
+        return [(gc.GROUP_PFD, 0, 32, zeta)]
+    if k == 4:
+        return [(gc.GROUP_AFOR, 0, 32, zeta)]
+    return [(gc.GROUP_SIMPLE, 0, 32, zeta), (gc.GROUP_SCHEME, gc.gsc_variant(1, "CU"), 32, zeta),
+            (gc.GROUP_SCHEME, gc.gsc_variant(8, "IU"), 32, zeta), (gc.GROUP_AFOR, 0, 32, zeta),
+            (gc.GROUP_PFD, 0, 32, zeta)]
+
+
+def make_workload(args, rank, world):
+    import gen
+    if args.config == 5:   # config 5 is defined sharded across 8 GPUs; rank r takes shard r
+        return gen.config(5, scale=args.scale, shard=rank % 8, n_shards=8)
+    return gen.config(args.config, scale=args.scale, replica=rank)
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x2: "applications_clocks_setting", 0x80: "hw_power_brake"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_ev = [], 0, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+            self.max_mhz = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= int(fn(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.nv:
+            self.th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b],
+                "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_decode launch from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(workload)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def cpu_oracle_rate(hbs, frac_lists: float, budget_s: float, threads: int):
+    """The oracle decoder as it stands (oracle/gc_oracle.c, gco_decode_batch with the d-gap
+    prefix sum) on the first `frac_lists` of every batch's lists, T host threads."""
+    import oracle as O
+    samples = []
+    for hb in hbs:
+        L = max(1, int(round(hb.n_lists * frac_lists)))
+        d = hb.as_dict()
+        sub = dict(d)
+        sub["list_n"] = d["list_n"][:L]
+        for k in ("ctrl_off", "data_off", "exc_off", "out_off"):
+            sub[k] = d[k][:L + 1]
+        sub["total_out"] = int(d["out_off"][L])
+        samples.append(sub)
+    n_sample = sum(s["total_out"] for s in samples)
+    outs = [np.empty(max(s["total_out"], 1), np.uint32) for s in samples]
+    reps, t_tot = 0, 0.0
+    while reps == 0 or (t_tot < budget_s and reps < 20):
+        t0 = time.perf_counter()
+        for s, o in zip(samples, outs):
+            O.decode_batch(s, dgaps=True, threads=threads, out=o)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    return n_sample * reps / t_tot, n_sample, reps, t_tot
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    from paper_1502_01916_b200 import gc
+    import oracle as O
+    O.build()
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    w = make_workload(args, 0, 1)
+    hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
+           for c, v, f, z in config_codecs(args.config, zeta)]
+    threads = len(os.sched_getaffinity(0))
+    frac = min(1.0, 2.0e6 / max(1, w.n_ints))     # ~2M ints per variant per step
+    for _ in range(args.warmup):
+        cpu_oracle_rate(hbs, frac, 0.0, threads)
+    t0 = time.perf_counter()
+    n_step = 0
+    for _ in range(args.steps):
+        _, n_step, _, _ = cpu_oracle_rate(hbs, frac, 0.0, threads)
+    dt = time.perf_counter() - t0
+    value = n_step * args.steps / dt
+    sample = (f"first {frac:.4f} of the lists of each of {len(hbs)} batches "
+              f"({n_step} ints per step)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {"workload": w.name, "n_ints": w.n_ints,
+                                        "n_lists": int(len(w.list_n)),
+                                        "codecs": [gc.codec_label(c, v, f) for c, v, f, _ in
+                                                   config_codecs(args.config, zeta)]},
+        "cpu_baseline": {"kind": "oracle", "cores": threads, "sample": sample, "value": value,
+                         "unit": "ints/s"},
+        "e2e": {"value": value, "unit": "ints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank, local_rank, world = dist_info()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    from paper_1502_01916_b200 import build
+    build.build()
+    from paper_1502_01916_b200 import gc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    codecs = config_codecs(args.config, zeta)
+    if args.codecs:
+        keep = set(args.codecs.split(","))
+        codecs = [c for c in codecs if gc.codec_label(c[0], c[1], c[2]) in keep]
+
+    # ---- inputs (untimed): generate, encode with the library's host encoder, copy to HBM
+    t_setup = time.perf_counter()
+    w = make_workload(args, rank, world)
+    hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
+           for c, v, f, z in codecs]
+    dbs = [gc.to_device(hb, dev) for hb in hbs]
+    n_ints = w.n_ints
+    out = torch.empty(max(n_ints, 4), dtype=torch.int32, device=dev)
+    wss = [gc.alloc_workspace(db, dev) for db in dbs]
+    stream = torch.cuda.current_stream(dev)
+    labels = [gc.codec_label(c, v, f) for c, v, f, _ in codecs]
+
+    # ---- parity gate (untimed): every variant bit-exact against the generator
+    verified = None
+    if not args.no_verify:
+        vals = torch.from_numpy(w.values.view(np.int32)).to(dev)
+        ln = torch.from_numpy(w.list_n.astype(np.int64)).to(dev)
+        starts = torch.cumsum(ln, 0) - ln
+        starts = starts[ln > 0]
+        verified = True
+        for lab, db, ws in zip(labels, dbs, wss):
+            gaps, _ = gc.decode(db, out=out, ws=ws)
+            ok_g = bool(torch.equal(gaps, vals)) if not w.delta else None
+            docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
+            st = gc.read_device_status(ws)
+            g = docs.clone()
+            g[1:] = docs[1:] - docs[:-1]
+            g[starts] = docs[starts]
+            ok = bool(torch.equal(docs, vals)) if w.delta else bool(torch.equal(g, vals))
+            if ok_g is False or not ok or st:
+                verified = False
+                print(f"[rank {rank}] PARITY FAILURE {lab}: gaps={ok_g} docs={ok} status="
+                      f"{gc.status_names(st)}", file=sys.stderr)
+        del vals
+    t_setup = time.perf_counter() - t_setup
+
+    # ---- timed region: K steps x all variants of gc_decode_dgaps (stage events per launch)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in dbs] for _ in range(args.steps)]
+
+    def step(evs=None):
+        for i, (db, ws) in enumerate(zip(dbs, wss)):
+            if evs is not None:
+                evs[i][0].record(stream)
+            gc.decode_stage(db, out, ws, True, gc.STAGE_RESET | gc.STAGE_INDEX, stream)
+            if evs is not None:
+                evs[i][1].record(stream)
+            gc.decode_stage(db, out, ws, True, gc.STAGE_DECODE, stream)
+            if evs is not None:
+                evs[i][2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    dec_ms = [sum(ev[k][i][1].elapsed_time(ev[k][i][2]) for k in range(args.steps)) / args.steps
+              for i in range(len(dbs))]
+    idx_ms = [sum(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)) / args.steps
+              for i in range(len(dbs))]
+
+    # ---- NCCL: max time over ranks; sum of counts / checksums / status (after timing)
+    status = 0
+    chk = np.zeros(3, np.uint64)
+    for db, ws in zip(dbs, wss):
+        docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
+        status |= gc.read_device_status(ws)
+        chk += gc.checksum(db, docs, list_base=rank * len(w.list_n)).cpu().numpy().view(np.uint64)
+    if pg:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+        s = torch.tensor([int(n_ints) * len(dbs), int(status), int(bool(verified))],
+                         dtype=torch.int64, device=dev)
+        pg.all_reduce(s)
+        c = torch.from_numpy(chk.view(np.int64).copy()).to(dev)
+        pg.all_reduce(c)
+        total_ints = int(s[0].item())
+        chk = c.cpu().numpy().view(np.uint64)
+        all_verified = None if verified is None else int(s[2].item()) == world
+    else:
+        total_ints = n_ints * len(dbs)
+        all_verified = verified
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    ints_per_step_all = total_ints
+    value = ints_per_step_all * args.steps / (ms / 1e3)
+    # ---- roofline of the dominant kernel (k_decode, all variants): algorithmic bytes =
+    # compressed stream bytes + 4 B per decoded int; directory excluded.
+    algo = [hb.compressed_bytes + 4 * hb.total_out for hb in hbs]
+    achieved = sum(algo) / (sum(dec_ms) / 1e3) / 1e9
+    peak, peak_src = peaks()
+    traffic = ncu_traffic(w.name)
+    per_codec = {}
+    for lab, hb, a, dm, im in zip(labels, hbs, algo, dec_ms, idx_ms):
+        per_codec[lab] = {
+            "ints_per_s": hb.total_out / ((dm + im) / 1e3),
+            "decode_kernel_ms": round(dm, 5), "index_ms": round(im, 5),
+            "bits_per_int": round(8 * hb.compressed_bytes / max(hb.total_out, 1), 3),
+            "decode_kernel_gbs": round(a / (dm / 1e3) / 1e9, 1),
+            "frac_of_peak": round(a / (dm / 1e3) / 1e9 / peak, 3),
+        }
+
+    # ---- e2e through the C ABI from pinned HOST buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pinned = []
+        for hb in hbs:
+            def pin(a):
+                t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+                v = t.numpy().view(a.dtype).reshape(a.shape)
+                v[...] = a
+                return t, v
+            keep, fields = [], {}
+            for k in ("list_n", "ctrl_off", "data_off", "exc_off", "out_off", "ctrl", "data", "exc"):
+                t, v = pin(getattr(hb, k))
+                keep.append(t)
+                fields[k] = v
+            phb = gc.HostBatch(hb.codec, hb.variant, hb.frame_quads, **fields)
+            pinned.append((phb, keep))
+        host_out_t = torch.empty(max(n_ints, 4) * 4, dtype=torch.uint8, pin_memory=True)
+        host_out = host_out_t.numpy().view(np.uint32)[:n_ints]
+        scratch = torch.empty(max(gc.host_scratch_size(p) for p, _ in pinned), dtype=torch.uint8,
+                              device=dev)
+        del dbs, wss, out
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            for phb, _ in pinned:
+                gc.decode_host(phb, host_out, True, scratch, stream)
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a0.elapsed_time(a1)
+        h2d = sum(p.directory_bytes + len(p.ctrl) + 16 * len(p.data) + len(p.exc) for p, _ in pinned)
+        e2e = {"value": n_ints * len(pinned) * args.e2e_steps / (ems / 1e3), "unit": "ints/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * n_ints * len(pinned)),
+               "steps": args.e2e_steps, "ms_per_step": ems / args.e2e_steps,
+               "api": "gc_decode_host (pinned host buffers)"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        O.build()
+        threads = len(os.sched_getaffinity(0))
+        frac = min(1.0, 8.0e6 / max(1, n_ints))
+        rate, n_sample, reps, t_cpu = cpu_oracle_rate(hbs, frac, 10.0, threads)
+        cpu = {"value": rate, "unit": "ints/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {frac:.4f} of the lists of all {len(hbs)} batches "
+                         f"({n_sample} ints), {reps} rep(s), {t_cpu:.1f} s, gco_decode_batch "
+                         "with the d-gap prefix sum"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": w.name, "n_ints_per_gpu": n_ints, "n_lists_per_gpu": int(len(w.list_n)),
+                   "codecs": labels, "ints_per_step_all_gpus": ints_per_step_all,
+                   "parallelism": f"dp{world} (lists sharded, weak)",
+                   "l2": "no flush: every variant's working set "
+                         f"({min(algo) / 1e6:.0f}-{max(algo) / 1e6:.0f} MB) exceeds the 126 MB L2",
+                   "path": "gc_decode_dgaps (index scan + fused decode/d-gap scan)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "k_decode (all variants)", "algorithmic_bytes_per_step": sum(algo)},
+        "per_codec": per_codec,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 2 * len(hbs) * args.steps,
+        "clocks": clk.summary(),
+        "parity": {"verified": all_verified, "device_status": status,
+                   "checksum": [int(x) for x in chk]},
+        "setup_s": round(t_setup, 1),
+    }
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

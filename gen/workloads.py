@@ -128,8 +128,8 @@ def _gaps_cfg2(list_n, seed, base=0):
     return np.where(pick < 0.7, geo, uni).astype(np.uint32)
 
 
-def _gaps_cfg3(n, seed):
-    lid = np.zeros(n, np.int64)
+def _gaps_cfg3(n, seed, replica=0):
+    lid = np.full(n, replica, np.int64)
     idx = np.arange(n, dtype=np.int64)
     exc = uniform01(seed, 31, lid, idx) < 0.08
     big = np.floor(2.0 ** (12.0 + 16.0 * uniform01(seed, 32, lid, idx))).astype(np.uint64)
@@ -159,31 +159,34 @@ CONFIGS = {
 }
 
 
-def config(k: int, scale: float = 1.0, shard: int = 0, n_shards: int = 1) -> Workload:
+def config(k: int, scale: float = 1.0, shard: int = 0, n_shards: int = 1,
+           replica: int = 0) -> Workload:
     """BASELINE.json configs[k-1].  `scale` < 1 shrinks totals (list counts scale too)
     for CPU-sized tests; `shard`/`n_shards` select a contiguous list range at the sum(n)
-    quantiles, each shard regenerated independently."""
+    quantiles, each shard regenerated independently.  `replica` r draws an
+    independent copy of the whole config (list ids offset by r*L in the RNG counters): the
+    per-GPU input of weak-scaling runs."""
     if k == 1:
         L, total = max(1, int(round(1000 * scale))), int(round((1 << 20) * scale))
         ln = zipf_lengths(L, total, 1.1, 16, 65536, seed=0)
         ln, base = _shard(ln, shard, n_shards)
-        return Workload("cfg1_group_simple", ln, uniform_subsets(ln, 1 << 24, 0, base), True, 0,
+        return Workload("cfg1_group_simple", ln, uniform_subsets(ln, 1 << 24, 0, base + replica * L), True, 0,
                         "1,000 lists, 2^20 docIDs in [0,2^24), Zipf(1.1) lengths in [16,65536]")
     if k == 2:
         L, total = max(1, int(round(100_000 * scale))), int(round((1 << 26) * scale))
         ln = zipf_lengths(L, total, 1.1, 1, 1 << 20, seed=1)
         ln, base = _shard(ln, shard, n_shards)
-        return Workload("cfg2_group_scheme", ln, _gaps_cfg2(ln, 1, base), False, 1,
+        return Workload("cfg2_group_scheme", ln, _gaps_cfg2(ln, 1, base + replica * L), False, 1,
                         "100k lists, 2^26 gaps: 0.7 Geom(0.05) + 0.3 U[1,2^16]")
     if k == 3:
         n = int(round((1 << 28) * scale))
-        return Workload("cfg3_group_pfd", np.array([n], np.uint32), _gaps_cfg3(n, 2), False, 2,
+        return Workload("cfg3_group_pfd", np.array([n], np.uint32), _gaps_cfg3(n, 2, replica), False, 2,
                         "one stream of 2^28 gaps: Geom(0.1) + 8% log-uniform [2^12,2^28)")
     if k == 4:
         L, total = max(1, int(round(1_000_000 * scale))), int(round((1 << 29) * scale))
         ln = zipf_lengths(L, total, 1.1, 1, 1 << 20, seed=3)
         ln, base = _shard(ln, shard, n_shards)
-        return Workload("cfg4_group_afor", ln, _gaps_cfg4(ln, 3, base), False, 3,
+        return Workload("cfg4_group_afor", ln, _gaps_cfg4(ln, 3, base + replica * L), False, 3,
                         "1M lists, 2^29 gaps: alternating runs gap=1 / Geom(0.001), run ~Geom(0.02)")
     if k == 5:
         L, total = max(1, int(round(50_000_000 * scale))), int(round((1 << 34) * scale))
