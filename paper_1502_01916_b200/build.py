@@ -16,7 +16,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES_CU = ["gc_kernels.cu"]
 SOURCES_CPP = ["gc_encoder.cpp"]
-HEADERS = ["gc_codecs.cuh", "gc_device.cuh"]
+HEADERS = ["gc_codecs.cuh", "gc_device.cuh", "gc_decode.cuh"]
 
 
 def _stale() -> bool:
@@ -29,14 +29,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()) -> str:
+    if not force and lib == LIB and not _stale():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     objs = []
     for f in SOURCES_CU:
-        o = os.path.join(BUILD, f + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        o = os.path.join(BUILD, f + "".join(d.replace("=", "") for d in defines) + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "186",
+               *[f"-D{d}" for d in defines],
                "-Xptxas", "-v" if verbose else "-O3", "-I", INC, "-I", CSRC, "-c",
                os.path.join(CSRC, f), "-o", o]
         subprocess.check_call(cmd)
@@ -47,11 +48,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
                os.path.join(CSRC, f), "-o", o]
         subprocess.check_call(cmd)
         objs.append(o)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv,
+                lib=out[0] if out else LIB, defines=defs))

@@ -79,6 +79,10 @@ struct CodecGS {
     for (int k = 0; k < 8; k++) q += gs_num((c.w >> (4 * k)) & 15u);  // low nibble first (A6)
     return WAgg{q, 8u * 32u, 0u};
   }
+  // may the word hold a malformed group?  (a nibble > 9: bit 3 and bit 2 or 1)
+  __device__ static bool suspect(const WCtx& c) {
+    return ((c.w >> 3) & ((c.w >> 2) | (c.w >> 1)) & 0x11111111u) != 0;
+  }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
     uint32_t q = 0;
@@ -121,6 +125,7 @@ struct CodecGscB {
     for (int k = 0; k < kFields; k++) d += CG * (field(c.w, k) + 1);  // Eq. (2)
     return WAgg{(uint32_t)kFields, d, 0u};
   }
+  __device__ static bool suspect(const WCtx&) { return false; }  // every field value is valid
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
     int32_t d = 0;
@@ -151,6 +156,19 @@ struct CodecGscCU {
   static constexpr bool kVectorGroups = false;
   __device__ static WAgg agg(const WCtx& c) {
     return WAgg{(uint32_t)__popc(~c.w), (uint32_t)(CG * 32), 0u};
+  }
+  // a run of >= 32/CG ones touching this word (stream order, previous word included)
+  __device__ static bool suspect(const WCtx& c) {
+    uint64_t x = ((uint64_t)(c.widx ? __byte_perm(c.prev, 0, 0x0123) : 0u) << 32) |
+                 __byte_perm(c.w, 0, 0x0123);
+    uint64_t y = x;
+    uint32_t have = 1;
+    while (have * 2 <= 32u / CG) {
+      y &= y >> have;
+      have *= 2;
+    }
+    if (have < 32u / CG) y &= y >> (32u / CG - have);
+    return (uint32_t)y != 0;
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
@@ -204,6 +222,19 @@ struct CodecGscIU {
       d += m ? CG * (9u - (uint32_t)__ffs(m)) : 0u;  // used bits = 8 - trailing ones
     }
     return WAgg{(uint32_t)__popc(~c.w), d, 0u};
+  }
+  // a byte without a 0, or a code of more than 32/CG units (padding ones excluded)
+  __device__ static bool suspect(const WCtx& c) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t b = (c.w >> (8 * i)) & 0xFFu;
+      if (b == 0xFFu) return true;
+      uint32_t t = b & (b + 1);  // clear the trailing (padding) ones
+      uint32_t y = t;
+      for (uint32_t r = 1; r < 32u / CG; r++) y &= t << r;
+      if (y & 0xFFu) return true;
+    }
+    return false;
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
@@ -263,6 +294,9 @@ struct CodecAFOR {
     }
     return WAgg{q, d, 0u};
   }
+  __device__ static bool suspect(const WCtx& c) {  // length code 3 or bit 7
+    return ((c.w & (c.w >> 1) & 0x01010101u) | (c.w & 0x80808080u)) != 0;
+  }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
     uint32_t q = 0;
@@ -318,6 +352,11 @@ struct CodecPFD {
     Grp g = grp0();
     decode_hdr(c, g);
     return WAgg{(uint32_t)F, g.dlen, g.elen};
+  }
+  __device__ static bool suspect(const WCtx& c) {
+    Grp g = grp0();
+    decode_hdr(c, g);
+    return g.err != 0;
   }
   template <class F2>
   __device__ static void walk(const WCtx& c, F2&& f) {

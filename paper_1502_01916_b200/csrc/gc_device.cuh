@@ -18,12 +18,12 @@ constexpr uint32_t kCA = kWA / kThreads;
 // Decode kernel (output-space tiles): tile t owns the quadruples that contain the
 // output positions [t*kT, (t+1)*kT).
 constexpr uint32_t kT = 4096;
-constexpr uint32_t kCB = 4;                      // control words per thread per parse round
-constexpr uint32_t kRoundWords = kCB * kThreads; // 1024
+constexpr uint32_t kCB = 2;                      // control words per thread per parse round
+constexpr uint32_t kRoundWords = kCB * kThreads; // 512
 constexpr uint32_t kRQ = 4 * kThreads;           // quads per unpack round (4 per thread)
 constexpr uint32_t kOutWords = kT + 8;           // staging window [t*kT-4, t*kT+kT+4)
 constexpr uint32_t kOutChunks = 1032;            // 16-B chunks incl. swizzle slack
-constexpr uint32_t kCCap = kRoundWords + 8;      // staged control words
+constexpr uint32_t kCCap = 1032;                 // staged control words (4 KiB + halo)
 constexpr uint32_t kDCap = 1280;                 // staged data vectors (20 KiB)
 constexpr uint32_t kECap = 4096;                 // staged exception bytes
 constexpr uint32_t kResetWords = kOutWords / 32 + 2;

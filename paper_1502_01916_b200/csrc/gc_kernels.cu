@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
   }
   __syncthreads();
 
-  // pass 2: walk the groups with their prefixes; write tile Entries; check bounds
+  // pass 2: per word, only where needed (a tile boundary falls in it, it is the list's
+  // last word, or a cheap test says it may be malformed), walk the groups: write the tile
+  // Entries and check the groups' bounds
   Seg3 S = seg3_op(s_prefix, excl);
   L = L0;
   uint32_t err = 0;
@@ -243,6 +245,19 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
     c.Q = L.Q;
     if (c.widx == 0) S = Seg3{1u, 0u, L.dbase, L.ebase};
     const Seg3 SW = S;
+    const WAgg a = C::agg(c);
+    S.q += a.q;
+    S.d += a.d;
+    S.e += a.e;
+    const bool last = w + 1 == L.cw_hi;
+    if (last && (uint64_t)S.q < L.Q) err |= GC_DEV_TRUNCATED;  // control ends before Q quads
+    const uint64_t qa = SW.q, qb = mn64((uint64_t)SW.q + a.q, L.Q);
+    bool boundary = false;
+    if (qb > qa) {
+      const uint64_t lo_int = L.oo + 4 * qa, hi_int = L.oo + mn64(4 * qb, L.n);
+      boundary = ((lo_int + kT - 1) / kT) * kT < hi_int;
+    }
+    if (!(boundary || last || C::suspect(c))) continue;
     C::walk(c, [&](const Grp& g) {
       uint64_t gq = (uint64_t)SW.q + g.q0;
       if (gq < L.Q && g.err) err |= g.err;
@@ -278,377 +293,13 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
         D.entries[t] = e;
       }
     });
-    WAgg a = C::agg(c);
-    S.q += a.q;
-    S.d += a.d;
-    S.e += a.e;
-    if (w + 1 == L.cw_hi && (uint64_t)S.q < L.Q) err |= GC_DEV_TRUNCATED;  // list not covered
   }
   report(&s_err, err);
   __syncthreads();
   if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
 }
 
-// =====================================================================================
-// k_decode (subsystems (b)-(d)): one output tile of kT ints per CTA.
-// =====================================================================================
-struct DecodeSmem {
-  static constexpr uint32_t kOutOff = 0;
-  static constexpr uint32_t kDescOff = kOutOff + kOutChunks * 16;
-  static constexpr uint32_t kDataOff = kDescOff + kRQ * 8;
-  static constexpr uint32_t kCtrlOff = kDataOff + kDCap * 16;
-  static constexpr uint32_t kExcOff = kCtrlOff + kCCap * 4;
-  static constexpr uint32_t kResetOff0 = kExcOff;
-  __host__ __device__ static constexpr uint32_t reset_off(bool exc) { return kExcOff + (exc ? kECap : 0); }
-  __host__ __device__ static constexpr uint32_t bytes(bool exc) { return reset_off(exc) + kResetWords * 4; }
-};
-
-template <class C, bool DGAPS>
-__global__ void __launch_bounds__(kThreads, 4) k_decode(Dev D, uint32_t* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint4* s_out4 = reinterpret_cast<uint4*>(smem + DecodeSmem::kOutOff);
-  uint32_t* s_out = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kOutOff);
-  uint2* s_desc = reinterpret_cast<uint2*>(smem + DecodeSmem::kDescOff);
-  uint4* s_data = reinterpret_cast<uint4*>(smem + DecodeSmem::kDataOff);
-  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kCtrlOff);
-  uint32_t* s_reset = reinterpret_cast<uint32_t*>(smem + DecodeSmem::reset_off(C::kExc));
-  uint8_t* s_exc = smem + DecodeSmem::kExcOff;
-
-  __shared__ Entry s_e0, s_e1;
-  __shared__ Seg3 s_scr3[kWarps];
-  __shared__ uint32_t s_scr1[kWarps];
-  __shared__ Seg1 s_scrs[kWarps];
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_tile, s_err, s_carry;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_tile = atomicAdd(&D.hdr->counter_b, 1u);
-    s_err = 0;
-    s_carry = 0;
-    const uint32_t t = s_tile;
-    s_e0 = D.entries[t];
-    if (t + 1 < D.n_tiles_b) {
-      s_e1 = D.entries[t + 1];
-    } else {
-      Entry e;
-      memset(&e, 0, sizeof(e));
-      e.l = (uint32_t)D.n_lists;
-      e.valid = 1;
-      e.cend = D.ctrl_off[D.n_lists] >> 2;
-      e.dend = D.data_off[D.n_lists] * 32ull;
-      e.eend = D.exc_off ? D.exc_off[D.n_lists] : 0ull;
-      s_e1 = e;
-    }
-    mbar_init(&s_bar, 1);
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const Entry E0 = s_e0, E1 = s_e1;
-  const int64_t base_int = (int64_t)tile * kT - 4;  // global int at staging index 0
-
-  if (!E0.valid || !E1.valid || E1.cend <= E0.gword || E0.l >= D.n_lists) {
-    if (tid == 0) {
-      atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
-      if (DGAPS) st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
-    }
-    return;
-  }
-
-  // ---- ranges of the three streams this tile needs
-  const uint64_t wa = E0.gword, wb = E1.cend;
-  const uint64_t cbase = (wa ? wa - 1 : 0) & ~3ull;
-  const uint64_t cstop = mn64((wb + 3) & ~3ull, D.n_ctrl_words);
-  const bool ctrl_staged = cstop - cbase <= kCCap;
-  const uint64_t va = E0.dbeg >> 5;
-  const uint64_t vb = mx64(va, mn64((E1.dend + 31) >> 5, D.data_vectors));
-  const bool data_staged = vb - va <= kDCap;
-  uint64_t ea = 0, eb = 0;
-  bool exc_staged = false;
-  if (C::kExc) {
-    ea = E0.ebeg & ~15ull;
-    eb = mx64(ea, mn64((E1.eend + 15) & ~15ull, D.exc_bytes));
-    exc_staged = eb - ea <= kECap;
-  }
-  if (tid == 0) {
-    uint32_t bytes = 0;
-    if (ctrl_staged && cstop > cbase) bytes += (uint32_t)(cstop - cbase) * 4;
-    if (data_staged && vb > va) bytes += (uint32_t)(vb - va) * 16;
-    if (C::kExc && exc_staged && eb > ea) bytes += (uint32_t)(eb - ea);
-    mbar_expect_tx(&s_bar, bytes);
-    if (ctrl_staged && cstop > cbase)
-      bulk_g2s(s_ctrl, D.ctrl_words + cbase, (uint32_t)(cstop - cbase) * 4, &s_bar);
-    if (data_staged && vb > va) bulk_g2s(s_data, D.data + va, (uint32_t)(vb - va) * 16, &s_bar);
-    if (C::kExc && exc_staged && eb > ea) bulk_g2s(s_exc, D.exc + ea, (uint32_t)(eb - ea), &s_bar);
-  }
-  const uint4* dptr = data_staged ? s_data : D.data + va;
-  const uint64_t dlim = vb - va;
-
-  // ---- output window of this tile
-  int64_t out_lo = (int64_t)(D.out_off[E0.l] + 4ull * E0.j);
-  int64_t out_hi = E1.l < D.n_lists ? (int64_t)(D.out_off[E1.l] + 4ull * E1.j) : (int64_t)D.total_out;
-  {
-    int64_t clo = smax64(base_int, 0), chi = smin64(base_int + kOutWords, (int64_t)D.total_out);
-    if (out_lo < clo || out_hi > chi || out_hi < out_lo) {
-      if (tid == 0) atomicOr(&s_err, (uint32_t)GC_DEV_TRUNCATED);
-      out_lo = smax64(out_lo, clo);
-      out_hi = smax64(out_lo, smin64(out_hi, chi));
-    }
-  }
-  const uint32_t lo_loc = (uint32_t)(out_lo - base_int), hi_loc = (uint32_t)(out_hi - base_int);
-  for (uint32_t i = tid; i < kResetWords; i += kThreads) s_reset[i] = 0;
-  for (uint32_t i = tid; i < lo_loc + (kOutWords - hi_loc); i += kThreads)
-    s_out[sw_word(i < lo_loc ? i : hi_loc + (i - lo_loc))] = 0;
-
-  mbar_wait(&s_bar, 0);
-  __syncthreads();
-
-  auto cword = [&](uint64_t w) -> uint32_t {
-    if (ctrl_staged) return (w >= cbase && w < cstop) ? s_ctrl[w - cbase] : 0u;
-    return w < D.n_ctrl_words ? D.ctrl_words[w] : 0u;
-  };
-  auto excb = [&](uint64_t b) -> uint32_t {
-    if (exc_staged) return (b >= ea && b < eb) ? s_exc[b - ea] : 0u;
-    return b < D.exc_bytes ? D.exc[b] : 0u;
-  };
-
-  uint32_t err = 0;
-  Seg3 carry{1u, E0.wq, E0.wd, E0.we};  // state at the start of word wa
-  const uint64_t lend = mn64((uint64_t)E1.l + 1, D.n_lists);
-
-  for (uint64_t r0 = wa; r0 < wb; r0 += kRoundWords) {
-    const uint64_t my0 = r0 + (uint64_t)tid * kCB;
-    const uint32_t myn = my0 < wb ? (uint32_t)mn64(kCB, wb - my0) : 0u;
-    ListCur L0;
-    L0.load(D, myn ? find_list(D.ctrl_off, E0.l, lend, 4 * my0) : D.n_lists);
-
-    // generic walk over my words: f(L, SW, c, g) per group; returns nothing
-    auto for_groups = [&](Seg3 S, auto&& f) {
-      ListCur L = L0;
-      for (uint32_t k = 0; k < myn; k++) {
-        uint64_t w = my0 + k;
-        L.seek(D, w);
-        if (L.l >= D.n_lists) break;
-        WCtx c;
-        c.w = cword(w);
-        c.prev = C::kNeedsPrev ? cword(w - 1) : 0u;
-        c.widx = w - L.cw_lo;
-        c.Q = L.Q;
-        if (c.widx == 0 && w != wa) S = Seg3{1u, 0u, L.dbase, L.ebase};
-        const Seg3 SW = S;
-        const uint64_t klo = L.l == E0.l ? E0.j : 0ull;
-        const uint64_t khi = mn64(L.Q, L.l == E1.l ? (uint64_t)E1.j : L.Q);
-        C::walk(c, [&](const Grp& g) {
-          uint64_t gq = (uint64_t)SW.q + g.q0;
-          uint64_t ka = mx64(gq, klo), kb = mn64(gq + g.nq, khi);
-          if (ka < kb) f(L, SW, g, gq, ka, kb);
-        });
-        WAgg a = C::agg(c);
-        S.q += a.q;
-        S.d += a.d;
-        S.e += a.e;
-      }
-    };
-
-    // pass 1: aggregates -> segmented block scan with the carry
-    Seg3 agg{0, 0, 0, 0};
-    {
-      ListCur L = L0;
-      for (uint32_t k = 0; k < myn; k++) {
-        uint64_t w = my0 + k;
-        L.seek(D, w);
-        if (L.l >= D.n_lists) break;
-        WCtx c;
-        c.w = cword(w);
-        c.prev = C::kNeedsPrev ? cword(w - 1) : 0u;
-        c.widx = w - L.cw_lo;
-        c.Q = L.Q;
-        WAgg a = C::agg(c);
-        Seg3 v = (c.widx == 0 && w != wa) ? Seg3{1u, a.q, L.dbase + a.d, L.ebase + a.e}
-                                          : Seg3{0u, a.q, a.d, a.e};
-        agg = seg3_op(agg, v);
-      }
-    }
-    Seg3 total;
-    Seg3 excl = block_excl_seg3(agg, s_scr3, &total);
-    const Seg3 S0 = seg3_op(carry, excl);
-    carry = seg3_op(carry, total);
-
-    // pass 2: kept quads -> local quad indices
-    uint32_t kept = 0;
-    for_groups(S0, [&](const ListCur&, const Seg3&, const Grp&, uint64_t, uint64_t ka,
-                       uint64_t kb) { kept += (uint32_t)(kb - ka); });
-    uint32_t K;
-    const uint32_t lq0 = block_excl_sum(kept, s_scr1, &K);
-
-    for (uint32_t u = 0; u < K; u += kRQ) {
-      // pass 3: descriptors of the quads [u, u+kRQ)
-      uint32_t x = lq0;
-      for_groups(S0, [&](const ListCur& L, const Seg3& SW, const Grp& g, uint64_t gq,
-                         uint64_t ka, uint64_t kb) {
-        uint32_t cnt = (uint32_t)(kb - ka);
-        if (x + cnt > u && x < u + kRQ) {
-          int64_t gbit = (int64_t)(SW.d + (int64_t)g.d0) - (int64_t)(va * 32);
-          for (uint64_t j = ka; j < kb; j++, x++) {
-            if (x < u || x >= u + kRQ) continue;
-            int64_t pos = gbit + (int64_t)((j - gq) * g.step);
-            int64_t op = (int64_t)(L.oo + 4 * j) - base_int;
-            uint32_t c = (uint32_t)mn64(4, L.n - 4 * j);
-            bool ok = pos >= 0 && op >= (int64_t)lo_loc && op + c <= (int64_t)hi_loc;
-            if (!ok) err |= GC_DEV_TRUNCATED;
-            s_desc[x - u] = make_uint2(ok ? (uint32_t)pos : 0xFFFFFFFFu,
-                                       g.bw | ((uint32_t)op << 6) | ((c - 1) << 19));
-            if (DGAPS && j == 0 && ok) atomicOr(&s_reset[op >> 5], 1u << (op & 31));
-          }
-        } else {
-          x += cnt;
-        }
-      });
-      __syncthreads();
-      // unpack: 4 consecutive quads per thread (thread-per-quad on the 4 vertical lanes)
-      const uint32_t nr = mn32(kRQ, K - u);
-#pragma unroll
-      for (int s = 0; s < 4; s++) {
-        uint32_t qi = 4 * tid + s;
-        if (qi >= nr) break;
-        uint2 d = s_desc[qi];
-        if (d.x == 0xFFFFFFFFu) continue;
-        uint32_t bw = d.y & 63u, op = (d.y >> 6) & 0x1FFFu, c = ((d.y >> 19) & 3u) + 1u;
-        uint32_t m = d.x >> 5, off = d.x & 31u;
-        bool straddle = off + bw > 32;
-        if (m >= dlim || (straddle && m + 1 >= dlim)) {
-          err |= GC_DEV_TRUNCATED;
-          continue;
-        }
-        uint4 v0 = dptr[m];
-        uint4 v1 = straddle ? dptr[m + 1] : make_uint4(0, 0, 0, 0);
-        uint32_t lo_len = straddle ? off + bw - 32 : 0u;
-        uint32_t mk = mask_bits(bw), ml = (1u << lo_len) - 1u;
-        // high part from the current vector, low part from the next (A3)
-        uint32_t x0 = (((v0.x >> off) << lo_len) | (v1.x & ml)) & mk;
-        uint32_t x1 = (((v0.y >> off) << lo_len) | (v1.y & ml)) & mk;
-        uint32_t x2 = (((v0.z >> off) << lo_len) | (v1.z & ml)) & mk;
-        uint32_t x3 = (((v0.w >> off) << lo_len) | (v1.w & ml)) & mk;
-        s_out[sw_word(op)] = x0;
-        if (c > 1) s_out[sw_word(op + 1)] = x1;
-        if (c > 2) s_out[sw_word(op + 2)] = x2;
-        if (c > 3) s_out[sw_word(op + 3)] = x3;
-      }
-      __syncthreads();
-    }
-
-    if (C::kExc) {
-      // Group-PFD step 3: write each exception into its slot, before the scan
-      for_groups(S0, [&](const ListCur& L, const Seg3& SW, const Grp& g, uint64_t gq,
-                         uint64_t ka, uint64_t kb) {
-        const uint32_t posb = (4 * g.nq <= 256) ? 1u : 2u;
-        const uint64_t e0 = SW.e + g.e0;
-        const uint32_t qf = (uint32_t)mn64(g.nq, L.Q - gq);
-        uint32_t prev = 0;
-        for (uint32_t i = 0; i < g.cnt; i++) {
-          uint32_t p = excb(e0 + (uint64_t)i * posb);
-          if (posb == 2) p |= excb(e0 + (uint64_t)i * posb + 1) << 8;
-          if (p >= 4 * qf || (i > 0 && p <= prev)) {
-            err |= GC_DEV_BAD_EXCEPTION;
-            break;
-          }
-          prev = p;
-          uint64_t j = gq + (p >> 2);
-          if (j < ka || j >= kb) continue;
-          uint64_t gi = 4 * j + (p & 3);
-          if (gi >= L.n) continue;
-          uint64_t vb0 = e0 + (uint64_t)g.cnt * posb + (uint64_t)i * g.wb;
-          uint32_t v = 0;
-          for (uint32_t t = 0; t < g.wb; t++) v |= excb(vb0 + t) << (8 * t);
-          int64_t op = (int64_t)(L.oo + gi) - base_int;
-          s_out[sw_word((uint32_t)op)] = v;
-        }
-      });
-      __syncthreads();
-    }
-  }
-
-  // ---- segmented d-gap inclusive scan: thread-serial, block, look-back
-  if (DGAPS) {
-    // thread i owns staging ints [4+16i, 20+16i); thread 0 also the head chunk [0,4)
-    const uint32_t c_first = tid == 0 ? 0u : 1u + 4u * tid;
-    const uint32_t nchunk = tid == 0 ? 5u : 4u;
-    uint32_t run = 0, fl = 0;
-    for (uint32_t s = 0; s < nchunk; s++) {
-      uint32_t c = c_first + s;
-      uint4 v = s_out4[sw_chunk(c)];
-      uint32_t rb = (s_reset[(4 * c) >> 5] >> ((4 * c) & 31)) & 15u;
-      uint32_t a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (rb & (1u << k)) {
-          run = a[k];
-          fl = 1;
-        } else {
-          run += a[k];
-        }
-      }
-    }
-    Seg1 tot;
-    Seg1 ex = block_excl_seg1(Seg1{fl, run}, s_scrs, &tot);
-    if (tid < 32) {
-      // the first segment continues a list begun in an earlier tile iff E0.j > 0
-      const bool need_carry = E0.j > 0;
-      if (tid == 0)
-        st_relaxed_u64(D.tiles_b + tile,
-                       ((uint64_t)((tot.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) | tot.v);
-      uint32_t cin = 0;
-      if (need_carry) {
-        cin = lookback_u32(D.tiles_b, tile);
-        if (tid == 0 && !tot.f)
-          st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + tot.v));
-      }
-      if (tid == 0) s_carry = cin;
-    }
-    __syncthreads();
-    uint32_t add = ex.v + (ex.f ? 0u : s_carry);
-    bool seen = false;
-    run = 0;
-    for (uint32_t s = 0; s < nchunk; s++) {
-      uint32_t c = c_first + s;
-      uint4 v = s_out4[sw_chunk(c)];
-      uint32_t rb = (s_reset[(4 * c) >> 5] >> ((4 * c) & 31)) & 15u;
-      uint32_t a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (rb & (1u << k)) {
-          run = a[k];
-          seen = true;
-        } else {
-          run += a[k];
-        }
-        a[k] = seen ? run : run + add;
-      }
-      s_out4[sw_chunk(c)] = make_uint4(a[0], a[1], a[2], a[3]);
-    }
-    __syncthreads();
-  }
-
-  // ---- coalesced 128-bit store of [out_lo, out_hi)
-  {
-    const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
-    const int64_t cb = base_int / 4;
-    for (int64_t c = c_lo + tid; c < c_hi; c += kThreads) {
-      uint4 v = s_out4[sw_chunk((uint32_t)(c - cb))];
-      int64_t g = 4 * c;
-      if (g >= out_lo && g + 4 <= out_hi) {
-        __stcs(reinterpret_cast<uint4*>(out + g), v);
-      } else {
-        uint32_t a[4] = {v.x, v.y, v.z, v.w};
-        for (int k = 0; k < 4; k++)
-          if (g + k >= out_lo && g + k < out_hi) out[g + k] = a[k];
-      }
-    }
-  }
-  report(&s_err, err);
-  __syncthreads();
-  if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
-}
+#include "gc_decode.cuh"
 
 // =====================================================================================
 // checksum (verification only, G7)

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgc.so")
+LIB_PATH = os.environ.get("GC_LIB") or os.path.join(_PKG, "libgc.so")
 
 GROUP_SIMPLE, GROUP_SCHEME, GROUP_AFOR, GROUP_PFD = 2, 3, 4, 5
 CODEC_NAMES = {GROUP_SIMPLE: "group_simple", GROUP_SCHEME: "group_scheme",
