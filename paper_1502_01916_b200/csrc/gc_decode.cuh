@@ -1,15 +1,17 @@
 // gc_decode.cuh -- k_decode (subsystems (b)-(d)); included inside namespace gcd by
 // gc_kernels.cu.  One CTA decodes one output tile of kT ints: the quadruples containing
-// the output positions [t*kT, (t+1)*kT).  All in-tile arithmetic is 32-bit and relative to
-// the tile's staged bases.
+// the output positions [t*kT, (t+1)*kT).  In-tile arithmetic is 32-bit and relative to the
+// tile's staged bases; the tile's lists live in a shared-memory table.
 
 struct DecodeSmem {
   static constexpr uint32_t kOut = 0;                             // swizzled staging window
-  static constexpr uint32_t kDesc = kOut + kOutChunks * 16;       // uint2 per quad of a round
+  static constexpr uint32_t kDesc = kOut + kOutChunks * 16;       // uint2 per quad of a window
   static constexpr uint32_t kData = kDesc + kRQ * 8;              // data vectors (+1 slack)
   static constexpr uint32_t kCtrl = kData + (kDCap + 1) * 16;     // control words
-  static constexpr uint32_t kXinfo = kCtrl + kCCap * 4;           // PFD: exception info per quad
-  __host__ __device__ static constexpr uint32_t exc_off() { return kXinfo + kRQ * 4; }
+  static constexpr uint32_t kLt = kCtrl + kCCap * 4;              // list table (SoA)
+  static constexpr uint32_t kLtFields = 9;
+  static constexpr uint32_t kXinfo = (kLt + kLtFields * (kLT + 1) * 4 + 15) & ~15u;  // PFD info
+  __host__ __device__ static constexpr uint32_t exc_off() { return (kXinfo + kRQ * 4 + 15) & ~15u; }
   __host__ __device__ static constexpr uint32_t bytes(bool exc) {
     return exc ? exc_off() + kECap : kXinfo;
   }
@@ -61,14 +63,12 @@ __device__ __forceinline__ St block_excl_st(St v, uint32_t* scr, St* total) {
   return st_op(wpre, ex);
 }
 
-// List cursor with tile-relative fields.
-struct TileList {
-  uint64_t l, cw_lo, cw_hi;
-  uint32_t n, Q;
-  uint32_t klo, kend;  // quads of this list owned by the tile: [klo, kend)
-  uint32_t oref;       // staging index of quad j's first int = oref + 4j (mod 2^32)
-  uint32_t dbase;      // staged data lane-bit of the list's first vector (lists after the first)
-  uint32_t ebase;      // staged exception byte of the list's first exception
+struct TileInfo {
+  uint64_t wa, wb, cbase, cstop, va, vb, ea, eb, lf, ll;
+  int64_t out_lo, out_hi;
+  uint64_t wd0, we0;
+  uint32_t lo_loc, hi_loc, dlim, elim, j0, j1, wq0, nlists;
+  uint32_t ctrl_staged, data_staged, exc_staged, ok;
 };
 
 #ifndef GC_DECODE_MINB
@@ -82,229 +82,238 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
   uint2* s_desc = reinterpret_cast<uint2*>(smem + DecodeSmem::kDesc);
   uint4* s_data = reinterpret_cast<uint4*>(smem + DecodeSmem::kData);
   uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kCtrl);
+  uint32_t* s_lt = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kLt);
+  uint32_t* lt_cw = s_lt + 0 * (kLT + 1);     // first control word (relative to cbase)
+  uint32_t* lt_q = s_lt + 1 * (kLT + 1);      // quads
+  uint32_t* lt_n = s_lt + 2 * (kLT + 1);      // ints
+  uint32_t* lt_klo = s_lt + 3 * (kLT + 1);    // first quad owned by the tile
+  uint32_t* lt_kend = s_lt + 4 * (kLT + 1);   // one past the last
+  uint32_t* lt_oref = s_lt + 5 * (kLT + 1);   // staging index of quad j = oref + 4j
+  uint32_t* lt_db = s_lt + 6 * (kLT + 1);     // staged data lane-bit of the list start
+  uint32_t* lt_eb = s_lt + 7 * (kLT + 1);     // staged exception byte of the list start
+  uint32_t* lt_lb = s_lt + 8 * (kLT + 1);     // local index of quad klo within the round
   uint32_t* s_xinfo = reinterpret_cast<uint32_t*>(smem + DecodeSmem::kXinfo);
   uint8_t* s_exc = smem + DecodeSmem::exc_off();
 
-  __shared__ Entry s_e0, s_e1;
+  __shared__ TileInfo s_ti;
   __shared__ uint32_t s_scr[kWarps * 4];
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint32_t s_tile, s_err, s_carry, s_reset0;
 
   const int tid = threadIdx.x;
+  // ---------------------------------------------------------------- tile setup (thread 0)
   if (tid == 0) {
-    s_tile = atomicAdd(&D.hdr->counter_b, 1u);
+    const uint32_t t = atomicAdd(&D.hdr->counter_b, 1u);
+    s_tile = t;
     s_err = 0;
     s_carry = 0;
-    const uint32_t t = s_tile;
-    s_e0 = D.entries[t];
+    TileInfo ti;
+    const Entry E0 = D.entries[t];
+    Entry E1;
     if (t + 1 < D.n_tiles_b) {
-      s_e1 = D.entries[t + 1];
+      E1 = D.entries[t + 1];
     } else {
-      Entry e;
-      memset(&e, 0, sizeof(e));
-      e.l = (uint32_t)D.n_lists;
-      e.valid = 1;
-      e.cend = D.ctrl_off[D.n_lists] >> 2;
-      e.dend = D.data_off[D.n_lists] * 32ull;
-      e.eend = D.exc_off ? D.exc_off[D.n_lists] : 0ull;
-      s_e1 = e;
+      E1.l = (uint32_t)D.n_lists;
+      E1.j = 0;
+      E1.valid = 1;
+      E1.cend = D.ctrl_off[D.n_lists] >> 2;
+      E1.dend = D.data_off[D.n_lists] * 32ull;
+      E1.eend = D.exc_off ? D.exc_off[D.n_lists] : 0ull;
     }
-    mbar_init(&s_bar, 1);
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const Entry E0 = s_e0, E1 = s_e1;
-  const int64_t base_int = (int64_t)tile * kT - 4;  // global int at staging index 0
-
-  if (!E0.valid || !E1.valid || E1.cend <= E0.gword || E0.l >= D.n_lists) {
-    if (tid == 0) {
+    ti.ok = E0.valid && E1.valid && E1.cend > E0.gword && E0.l < D.n_lists;
+    if (ti.ok) {
+      const int64_t base_int = (int64_t)t * kT - 4;
+      ti.wa = E0.gword;
+      ti.wb = E1.cend;
+      ti.cbase = (ti.wa ? ti.wa - 1 : 0) & ~3ull;
+      ti.cstop = mn64((ti.wb + 3) & ~3ull, D.n_ctrl_words);
+      ti.ctrl_staged = ti.cstop - ti.cbase <= kCCap;
+      ti.va = E0.dbeg >> 5;
+      ti.vb = mx64(ti.va, mn64((E1.dend + 31) >> 5, D.data_vectors));
+      ti.data_staged = ti.vb - ti.va <= kDCap;
+      ti.ea = ti.eb = 0;
+      ti.exc_staged = 0;
+      if (C::kExc) {
+        ti.ea = E0.ebeg & ~15ull;
+        ti.eb = mx64(ti.ea, mn64((E1.eend + 15) & ~15ull, D.exc_bytes));
+        ti.exc_staged = ti.eb - ti.ea <= kECap;
+      }
+      ti.dlim = (uint32_t)mn64(ti.vb - ti.va, 0x7FFFFFFFull);
+      ti.elim = (uint32_t)mn64(ti.eb - ti.ea, 0x7FFFFFFFull);
+      uint32_t bytes = 0;
+      if (ti.ctrl_staged && ti.cstop > ti.cbase) bytes += (uint32_t)(ti.cstop - ti.cbase) * 4;
+      if (ti.data_staged && ti.vb > ti.va) bytes += (uint32_t)(ti.vb - ti.va) * 16;
+      if (C::kExc && ti.exc_staged && ti.eb > ti.ea) bytes += (uint32_t)(ti.eb - ti.ea);
+      mbar_init(&s_bar, 1);
+      mbar_expect_tx(&s_bar, bytes);
+      if (ti.ctrl_staged && ti.cstop > ti.cbase)
+        bulk_g2s(s_ctrl, D.ctrl_words + ti.cbase, (uint32_t)(ti.cstop - ti.cbase) * 4, &s_bar);
+      if (ti.data_staged && ti.vb > ti.va)
+        bulk_g2s(s_data, D.data + ti.va, (uint32_t)(ti.vb - ti.va) * 16, &s_bar);
+      if (C::kExc && ti.exc_staged && ti.eb > ti.ea)
+        bulk_g2s(s_exc, D.exc + ti.ea, (uint32_t)(ti.eb - ti.ea), &s_bar);
+      int64_t out_lo = (int64_t)(D.out_off[E0.l] + 4ull * E0.j);
+      int64_t out_hi =
+          E1.l < D.n_lists ? (int64_t)(D.out_off[E1.l] + 4ull * E1.j) : (int64_t)D.total_out;
+      const int64_t clo = smax64(base_int, 0);
+      const int64_t chi = smin64(base_int + kOutWords, (int64_t)D.total_out);
+      if (out_lo < clo || out_hi > chi || out_hi < out_lo) {
+        s_err = GC_DEV_TRUNCATED;
+        out_lo = smax64(out_lo, clo);
+        out_hi = smax64(out_lo, smin64(out_hi, chi));
+      }
+      ti.out_lo = out_lo;
+      ti.out_hi = out_hi;
+      ti.lo_loc = (uint32_t)(out_lo - base_int);
+      ti.hi_loc = (uint32_t)(out_hi - base_int);
+      ti.lf = E0.l;
+      ti.ll = E1.l;
+      ti.j0 = E0.j;
+      ti.j1 = E1.j;
+      ti.wq0 = E0.wq;
+      ti.wd0 = E0.wd;
+      ti.we0 = E0.we;
+      const uint64_t lend = E1.j > 0 && E1.l < D.n_lists ? (uint64_t)E1.l + 1 : (uint64_t)E1.l;
+      ti.nlists = (uint32_t)(lend - E0.l);
+      s_reset0 = ti.hi_loc;
+    } else {
       atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
-      if (DGAPS) st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
+      if (DGAPS) st_relaxed_u64(D.tiles_b + t, ((uint64_t)kFlagIncl << 32));
     }
-    return;
+    s_ti = ti;
   }
-
-  // ---- the three stream ranges of this tile -> shared memory (bulk async copies)
-  const uint64_t wa = E0.gword, wb = E1.cend;
-  const uint64_t cbase = (wa ? wa - 1 : 0) & ~3ull;
-  const uint64_t cstop = mn64((wb + 3) & ~3ull, D.n_ctrl_words);
-  const bool ctrl_staged = cstop - cbase <= kCCap;
-  const uint64_t va = E0.dbeg >> 5;
-  const uint64_t vb = mx64(va, mn64((E1.dend + 31) >> 5, D.data_vectors));
-  const bool data_staged = vb - va <= kDCap;
-  uint64_t ea = 0, eb = 0;
-  bool exc_staged = false;
-  if (C::kExc) {
-    ea = E0.ebeg & ~15ull;
-    eb = mx64(ea, mn64((E1.eend + 15) & ~15ull, D.exc_bytes));
-    exc_staged = eb - ea <= kECap;
-  }
-  if (tid == 0) {
-    uint32_t bytes = 0;
-    if (ctrl_staged && cstop > cbase) bytes += (uint32_t)(cstop - cbase) * 4;
-    if (data_staged && vb > va) bytes += (uint32_t)(vb - va) * 16;
-    if (C::kExc && exc_staged && eb > ea) bytes += (uint32_t)(eb - ea);
-    mbar_expect_tx(&s_bar, bytes);
-    if (ctrl_staged && cstop > cbase)
-      bulk_g2s(s_ctrl, D.ctrl_words + cbase, (uint32_t)(cstop - cbase) * 4, &s_bar);
-    if (data_staged && vb > va) bulk_g2s(s_data, D.data + va, (uint32_t)(vb - va) * 16, &s_bar);
-    if (C::kExc && exc_staged && eb > ea) bulk_g2s(s_exc, D.exc + ea, (uint32_t)(eb - ea), &s_bar);
-  }
-  const uint32_t* cwp = ctrl_staged ? s_ctrl : D.ctrl_words + cbase;  // word w at cwp[w-cbase]
-  const uint4* dptr = data_staged ? s_data : D.data + va;
-  const uint8_t* eptr = exc_staged ? s_exc : D.exc + ea;
-  const uint32_t dlim = (uint32_t)mn64(vb - va, 0x7FFFFFFFull);
-  const uint32_t elim = (uint32_t)mn64(eb - ea, 0x7FFFFFFFull);
-
-  // ---- output window
-  int64_t out_lo = (int64_t)(D.out_off[E0.l] + 4ull * E0.j);
-  int64_t out_hi = E1.l < D.n_lists ? (int64_t)(D.out_off[E1.l] + 4ull * E1.j) : (int64_t)D.total_out;
-  {
-    int64_t clo = smax64(base_int, 0), chi = smin64(base_int + kOutWords, (int64_t)D.total_out);
-    if (out_lo < clo || out_hi > chi || out_hi < out_lo) {
-      if (tid == 0) atomicOr(&s_err, (uint32_t)GC_DEV_TRUNCATED);
-      out_lo = smax64(out_lo, clo);
-      out_hi = smax64(out_lo, smin64(out_hi, chi));
-    }
-  }
-  const uint32_t lo_loc = (uint32_t)(out_lo - base_int), hi_loc = (uint32_t)(out_hi - base_int);
-  if (tid == 0) s_reset0 = hi_loc;
-
-  const uint64_t lf = E0.l, ll = E1.l;
-  const uint32_t oref_first = lo_loc - 4u * E0.j;
-  auto load_list = [&](TileList& L, uint64_t li) {
-    L.l = li;
-    if (li >= D.n_lists) {
-      L.cw_lo = L.cw_hi = ~0ull;
-      L.n = L.Q = L.klo = L.kend = 0;
-      return;
-    }
-    L.cw_lo = D.ctrl_off[li] >> 2;
-    L.cw_hi = D.ctrl_off[li + 1] >> 2;
-    L.n = D.list_n[li];
-    L.Q = (L.n + 3) >> 2;
-    L.klo = li == lf ? E0.j : 0u;
-    L.kend = li == ll ? mn32(L.Q, E1.j) : L.Q;
-    L.oref = li == lf ? oref_first : (uint32_t)((int64_t)D.out_off[li] - base_int);
-    L.dbase = (uint32_t)(D.data_off[li] * 32ull - va * 32ull);
-    L.ebase = C::kExc ? (uint32_t)(D.exc_off[li] - ea) : 0u;
-  };
-  auto seek = [&](TileList& L, uint64_t w) {
-    if (L.l < D.n_lists && w < L.cw_hi) return;
-    uint64_t li = L.l;
-    while (li < D.n_lists && (D.ctrl_off[li + 1] >> 2) <= w) li++;
-    load_list(L, li);
-  };
-
-  mbar_wait(&s_bar, 0);
   __syncthreads();
+  if (!s_ti.ok) return;
+  const uint32_t tile = s_tile;
+  const int64_t base_int = (int64_t)tile * kT - 4;
+  const uint64_t wa = s_ti.wa, wb = s_ti.wb, cbase = s_ti.cbase;
+  const uint64_t va = s_ti.va, ea = s_ti.ea;
+  const uint32_t dlim = s_ti.dlim, elim = s_ti.elim;
+  const uint32_t lo_loc = s_ti.lo_loc, hi_loc = s_ti.hi_loc;
+  const uint32_t ncw = (uint32_t)(s_ti.cstop - cbase);
+  const uint32_t* cwp = s_ti.ctrl_staged ? s_ctrl : D.ctrl_words + cbase;  // word w: cwp[w-cbase]
+  const uint4* dptr = s_ti.data_staged ? s_data : D.data + va;
+  const uint8_t* eptr = s_ti.exc_staged ? s_exc : D.exc + ea;
+  const uint64_t lf = s_ti.lf;
+  const uint32_t nlists = s_ti.nlists;
 
   uint32_t err = 0;
-  St carry{1u, E0.wq, (uint32_t)(E0.wd - va * 32ull), (uint32_t)(E0.we - ea)};
-  Seg1 rcarry{0u, 0u};  // d-gap running state across rounds
-  const uint64_t lsearch_hi = mn64(ll + 1, D.n_lists);
+  Seg1 rcarry{0u, 0u};  // d-gap running state across windows
+  bool staged_waited = false;
 
-  for (uint64_t r0 = wa; r0 < wb; r0 += kRoundWords) {
-    const uint64_t my0 = r0 + (uint64_t)tid * kCB;
-    const uint32_t myn = my0 < wb ? (uint32_t)mn64(kCB, wb - my0) : 0u;
-    TileList L0;
-    load_list(L0, myn ? find_list(D.ctrl_off, lf, lsearch_hi, 4 * my0) : D.n_lists);
-    uint32_t wv[kCB], pv[kCB];
-#pragma unroll
-    for (uint32_t k = 0; k < kCB; k++) {
-      uint64_t w = my0 + k;
-      wv[k] = (k < myn && w - cbase < cstop - cbase) ? cwp[w - cbase] : 0u;
-      pv[k] = (C::kNeedsPrev && k < myn && w > cbase) ? cwp[w - 1 - cbase] : 0u;
-    }
-
-    // pass 1: per-word aggregates, segmented scan with the tile carry
-    St agg{0, 0, 0, 0};
-    {
-      TileList L = L0;
-#pragma unroll
-      for (uint32_t k = 0; k < kCB; k++) {
-        if (k >= myn) break;
-        uint64_t w = my0 + k;
-        seek(L, w);
-        if (L.l >= D.n_lists) break;
-        WCtx c{wv[k], pv[k], w - L.cw_lo, L.Q};
-        WAgg a = C::agg(c);
-        if (c.widx == 0 && w != wa)
-          agg = St{1u, a.q, L.dbase + a.d, L.ebase + a.e};
-        else
-          agg = St{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
-      }
-    }
-    St rtot;
-    const St S0 = st_op(carry, block_excl_st<C::kExc>(agg, s_scr, &rtot));
-    carry = st_op(carry, rtot);
-
-    // pass 2: quads each word contributes to the tile -> local quad indices
+  for (uint32_t lr = 0; lr < nlists; lr += kLT) {
+    // ---------------------------------------------------------------- list table
+    const uint32_t cnt = min(kLT, nlists - lr);
     uint32_t kept = 0;
-    {
-      TileList L = L0;
-      St S = S0;
-#pragma unroll
-      for (uint32_t k = 0; k < kCB; k++) {
-        if (k >= myn) break;
-        uint64_t w = my0 + k;
-        seek(L, w);
-        if (L.l >= D.n_lists) break;
-        WCtx c{wv[k], pv[k], w - L.cw_lo, L.Q};
-        if (c.widx == 0 && w != wa) S = St{1u, 0u, L.dbase, L.ebase};
-        WAgg a = C::agg(c);
-        uint32_t qa = max(S.q, L.klo), qb = min(S.q + a.q, L.kend);
-        kept += qb > qa ? qb - qa : 0u;
-        S.q += a.q;
-        S.d += a.d;
-        S.e += a.e;
+    if ((uint32_t)tid <= cnt) {
+      const uint64_t l = lf + lr + tid;
+      const uint64_t cw = D.ctrl_off[mn64(l, D.n_lists)] >> 2;
+      lt_cw[tid] = (uint32_t)(cw - cbase);
+      if ((uint32_t)tid < cnt) {
+        const uint32_t n = D.list_n[l];
+        const uint32_t Q = (n + 3) >> 2;
+        const uint32_t klo = l == lf ? s_ti.j0 : 0u;
+        const uint32_t kend = l == s_ti.ll ? min(Q, s_ti.j1) : Q;
+        lt_q[tid] = Q;
+        lt_n[tid] = n;
+        lt_klo[tid] = klo;
+        lt_kend[tid] = kend;
+        lt_oref[tid] = l == lf ? lo_loc - 4u * s_ti.j0 : (uint32_t)((int64_t)D.out_off[l] - base_int);
+        lt_db[tid] = (uint32_t)(D.data_off[l] * 32ull - va * 32ull);
+        lt_eb[tid] = C::kExc ? (uint32_t)(D.exc_off[l] - ea) : 0u;
+        kept = kend > klo ? kend - klo : 0u;
       }
     }
     uint32_t K;
-    const uint32_t lq0 = block_excl_sum(kept, s_scr, &K);
+    const uint32_t lbk = block_excl_sum(kept, s_scr, &K);
+    if ((uint32_t)tid < cnt) lt_lb[tid] = lbk;
+    if (!staged_waited) {
+      mbar_wait(&s_bar, 0);
+      staged_waited = true;
+    }
+    __syncthreads();
+
+    // words of this list round
+    const uint64_t rw0 = lr == 0 ? wa : cbase + lt_cw[0];
+    const uint64_t rw1 = mn64(wb, cbase + lt_cw[cnt]);
 
     for (uint32_t u = 0; u < K; u += kRQ) {
-      // pass 3: per-quad descriptors (position, width, output slot) for quads [u, u+kRQ)
-      if (kept) {
-        TileList L = L0;
-        St S = S0;
-        uint32_t x = lq0;
+      St carry{1u, s_ti.wq0, (uint32_t)(s_ti.wd0 - va * 32ull), (uint32_t)(s_ti.we0 - ea)};
+      for (uint64_t r0 = rw0; r0 < rw1; r0 += kRoundWords) {
+        const uint64_t my0 = r0 + (uint64_t)tid * kCB;
+        const uint32_t myn = my0 < rw1 ? (uint32_t)mn64(kCB, rw1 - my0) : 0u;
+        // list of my first word: the last table entry whose first word is <= it
+        uint32_t li = 0;
+        if (myn) {
+          const uint32_t key = (uint32_t)(my0 - cbase);
+          uint32_t a = 0, b = cnt;
+          while (b - a > 1) {
+            const uint32_t m = (a + b) >> 1;
+            if (lt_cw[m] <= key) a = m;
+            else b = m;
+          }
+          li = a;
+        }
+        uint32_t wv[kCB], pv[kCB], wl[kCB];
+        St agg{0, 0, 0, 0};
+#pragma unroll
+        for (uint32_t k = 0; k < kCB; k++) {
+          const uint64_t w = my0 + k;
+          const uint32_t wr = (uint32_t)(w - cbase);
+          while (li + 1 < cnt && lt_cw[li + 1] <= wr) li++;
+          wl[k] = li;
+          wv[k] = (k < myn && wr < ncw) ? cwp[wr] : 0u;
+          pv[k] = (C::kNeedsPrev && k < myn && wr >= 1 && wr - 1 < ncw) ? cwp[wr - 1] : 0u;
+          if (k < myn) {
+            const uint32_t widx = wr - lt_cw[li];
+            WCtx c{wv[k], pv[k], widx, lt_q[li]};
+            const WAgg a = C::agg(c);
+            agg = (widx == 0 && w != wa) ? St{1u, a.q, lt_db[li] + a.d, lt_eb[li] + a.e}
+                                         : St{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
+          }
+        }
+        St rtot;
+        St S = st_op(carry, block_excl_st<C::kExc>(agg, s_scr, &rtot));
+        carry = st_op(carry, rtot);
+
+        // per-quad descriptors (position, width, staging slot) of the window's quads
 #pragma unroll
         for (uint32_t k = 0; k < kCB; k++) {
           if (k >= myn) break;
-          uint64_t w = my0 + k;
-          seek(L, w);
-          if (L.l >= D.n_lists) break;
-          WCtx c{wv[k], pv[k], w - L.cw_lo, L.Q};
-          if (c.widx == 0 && w != wa) S = St{1u, 0u, L.dbase, L.ebase};
-          WAgg a = C::agg(c);
-          const uint32_t qa = max(S.q, L.klo), qb = min(S.q + a.q, L.kend);
-          const uint32_t nk = qb > qa ? qb - qa : 0u;
-          if (nk && x < u + kRQ && x + nk > u) {
+          const uint64_t w = my0 + k;
+          const uint32_t wr = (uint32_t)(w - cbase);
+          const uint32_t i = wl[k];
+          const uint32_t widx = wr - lt_cw[i];
+          WCtx c{wv[k], pv[k], widx, lt_q[i]};
+          if (widx == 0 && w != wa) S = St{1u, 0u, lt_db[i], lt_eb[i]};
+          const WAgg a = C::agg(c);
+          const uint32_t klo = lt_klo[i], kend = lt_kend[i];
+          const uint32_t qa = max(S.q, klo), qb = min(S.q + a.q, kend);
+          const uint32_t x0 = lt_lb[i] + (qa - klo);  // local index of quad qa
+          if (qb > qa && x0 < u + kRQ && x0 + (qb - qa) > u) {
             const St SW = S;
-            const uint32_t xw = x;
+            const uint32_t n = lt_n[i], oref = lt_oref[i], Qi = lt_q[i];
             C::walk(c, [&](const Grp& g) {
               const uint32_t gq = SW.q + g.q0;
-              const uint32_t ja = max(max(gq, qa), qa + (u > xw ? u - xw : 0u));
-              const uint32_t jb = min(min(gq + g.nq, qb), qa + (u + kRQ - xw));
+              const uint32_t ja = max(max(gq, qa), qa + (u > x0 ? u - x0 : 0u));
+              const uint32_t jb = min(min(gq + g.nq, qb), qa + (u + kRQ - x0));
               if (ja >= jb) return;
               const uint32_t gd = SW.d + (uint32_t)g.d0;
-              uint32_t ei = 0, erank = 0;
-              uint32_t pprev = 0;
-              const uint32_t qf = C::kExc ? min(g.nq, L.Q - gq) : 0u;
+              uint32_t ei = 0, erank = 0, pprev = 0;
+              const uint32_t qf = C::kExc ? min(g.nq, Qi - gq) : 0u;
               for (uint32_t j = ja; j < jb; j++) {
-                const uint32_t loc = xw + (j - qa) - u;
-                const uint32_t pos = gd + (j - gq) * g.step;
-                const uint32_t op = L.oref + 4u * j;
-                const uint32_t cnt = min(4u, L.n - 4u * j);
+                const uint32_t loc = x0 + (j - qa) - u;
+                const uint32_t op = oref + 4u * j;
+                const uint32_t cq = min(4u, n - 4u * j);
                 const uint32_t rst = j == 0 ? 1u : 0u;
-                if (op + cnt > hi_loc || op < lo_loc) err |= GC_DEV_TRUNCATED;
-                s_desc[loc] = make_uint2(pos, g.bw | (min(op, kOutWords - 4) << 6) |
-                                                  ((cnt - 1) << 19) | (rst << 21));
+                if (op + cq > hi_loc || op < lo_loc) err |= GC_DEV_TRUNCATED;
+                s_desc[loc] = make_uint2(gd + (j - gq) * g.step,
+                                         g.bw | (min(op, kOutWords - 4) << 6) | ((cq - 1) << 19) |
+                                             (rst << 21));
                 if (DGAPS && rst) atomicMin(&s_reset0, op);
                 if (C::kExc) {
-                  // exceptions of this quad: positions [4t, 4t+4) of the frame
-                  const uint32_t t = j - gq;
+                  // exceptions of this quad: frame positions [4t, 4t+4)
+                  const uint32_t t4 = 4 * (j - gq);
                   const uint32_t pb = 4 * g.nq <= 256 ? 1u : 2u;
                   const uint32_t e0 = SW.e + g.e0;
                   uint32_t mask = 0;
@@ -321,21 +330,20 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
                       ei = g.cnt;
                       break;
                     }
-                    if (p >= 4 * t + 4) break;
+                    if (p >= t4 + 4) break;
                     pprev = p;
-                    if (p >= 4 * t) mask |= 1u << (p - 4 * t);
+                    if (p >= t4) mask |= 1u << (p - t4);
                     else erank++;
                     ei++;
                   }
                   const uint32_t wbc = g.wb == 1 ? 1u : (g.wb == 2 ? 2u : 3u);
-                  s_xinfo[loc] = mask ? (((e0 + g.cnt * pb + erank * g.wb) << 6) | (wbc << 4) | mask)
-                                      : 0u;
+                  s_xinfo[loc] =
+                      mask ? (((e0 + g.cnt * pb + erank * g.wb) << 6) | (wbc << 4) | mask) : 0u;
                   erank += __popc(mask);
                 }
               }
             });
           }
-          x += nk;
           S.q += a.q;
           S.d += a.d;
           S.e += a.e;
@@ -343,14 +351,15 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       }
       __syncthreads();
 
-      // unpack 4 consecutive quads per thread: shift/mask over the 4 vertical lanes, the
-      // high part of a straddling value from the current vector
+      // ---------------------------------------------------------------- unpack + d-gap scan
+      // kQPT consecutive quads per thread: shift/mask over the 4 vertical lanes, the high
+      // part of a straddling value from the current vector
       const uint32_t nr = min(kRQ, K - u);
-      uint32_t y[16], opq[4], cq[4];
-      uint32_t rsts = 0, run = 0, fl = 0;
+      uint32_t y[4 * kQPT], opq[kQPT], cqs = 0, rsts = 0;
+      uint32_t run = 0, fl = 0;
 #pragma unroll
-      for (int s = 0; s < 4; s++) {
-        const uint32_t qi = 4 * tid + s;
+      for (uint32_t s = 0; s < kQPT; s++) {
+        const uint32_t qi = kQPT * tid + s;
         uint32_t xq[4] = {0, 0, 0, 0};
         uint32_t op = 0, c = 0, rst = 0;
         if (qi < nr) {
@@ -398,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
           }
         }
         opq[s] = op;
-        cq[s] = c;
+        cqs |= c << (3 * s);
         rsts |= rst << s;
 #pragma unroll
         for (int k = 0; k < 4; k++) {
@@ -418,12 +427,12 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       }
       if (DGAPS) {
         Seg1 rt;
-        const Seg1 ex = seg1_op(rcarry, block_excl_seg1(Seg1{fl, run}, reinterpret_cast<Seg1*>(s_scr), &rt));
+        const Seg1 ex =
+            seg1_op(rcarry, block_excl_seg1(Seg1{fl, run}, reinterpret_cast<Seg1*>(s_scr), &rt));
         rcarry = seg1_op(rcarry, rt);
-        // values before this thread's first list start continue the running prefix
-        bool seen = false;
+        bool seen = false;  // values before this thread's first list start continue the prefix
 #pragma unroll
-        for (int s = 0; s < 4; s++) {
+        for (uint32_t s = 0; s < kQPT; s++) {
           if ((rsts >> s) & 1u) seen = true;
 #pragma unroll
           for (int k = 0; k < 4; k++)
@@ -431,22 +440,25 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
         }
       }
 #pragma unroll
-      for (int s = 0; s < 4; s++) {
+      for (uint32_t s = 0; s < kQPT; s++) {
+        const uint32_t c = (cqs >> (3 * s)) & 7u;
 #pragma unroll
         for (int k = 0; k < 4; k++)
-          if ((uint32_t)k < cq[s]) s_out[sw_word(opq[s] + k)] = y[4 * s + k];
+          if ((uint32_t)k < c) s_out[sw_word(opq[s] + k)] = y[4 * s + k];
       }
       __syncthreads();
     }
   }
+  if (!staged_waited) mbar_wait(&s_bar, 0);
 
-  // ---- d-gap look-back across tiles (segmented by list)
+  // ---------------------------------------------------------------- look-back
   if (DGAPS) {
     if (tid < 32) {
-      const bool need_carry = E0.j > 0;  // the tile's first quad continues a list
+      const bool need_carry = s_ti.j0 > 0;  // the tile's first quad continues a list
       if (tid == 0)
-        st_relaxed_u64(D.tiles_b + tile, ((uint64_t)((rcarry.f || !need_carry) ? kFlagIncl : kFlagAgg)
-                                          << 32) | rcarry.v);
+        st_relaxed_u64(D.tiles_b + tile,
+                       ((uint64_t)((rcarry.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) |
+                           rcarry.v);
       uint32_t cin = 0;
       if (need_carry) {
         cin = lookback_u32(D.tiles_b, tile);
@@ -458,11 +470,13 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
     __syncthreads();
   }
 
-  // ---- coalesced 128-bit store of [out_lo, out_hi); the tile's first list segment
-  // (before the first list start) gets the carry from the look-back
+  // ---------------------------------------------------------------- coalesced store
+  // 128-bit stores of [out_lo, out_hi); the tile's first list segment (before its first
+  // list start) gets the carry from the look-back
   {
     const uint32_t cin = DGAPS ? s_carry : 0u;
     const uint32_t r0loc = DGAPS ? s_reset0 : 0u;
+    const int64_t out_lo = s_ti.out_lo, out_hi = s_ti.out_hi;
     const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
     const int64_t cb = base_int / 4;
     for (int64_t c = c_lo + tid; c < c_hi; c += kThreads) {
@@ -470,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       uint4 v = s_out4[sw_chunk(lc)];
       if (DGAPS && cin) {
         const uint32_t p = 4 * lc;
-        if (p + 0 < r0loc) v.x += cin;
+        if (p < r0loc) v.x += cin;
         if (p + 1 < r0loc) v.y += cin;
         if (p + 2 < r0loc) v.z += cin;
         if (p + 3 < r0loc) v.w += cin;

@@ -20,12 +20,14 @@ constexpr uint32_t kCA = kWA / kThreads;
 constexpr uint32_t kT = 4096;
 constexpr uint32_t kCB = 2;                      // control words per thread per parse round
 constexpr uint32_t kRoundWords = kCB * kThreads; // 512
-constexpr uint32_t kRQ = 4 * kThreads;           // quads per unpack round (4 per thread)
+constexpr uint32_t kQPT = 5;                     // quads per thread per unpack window
+constexpr uint32_t kRQ = kQPT * kThreads;        // quads per unpack window (1280)
+constexpr uint32_t kLT = 128;                    // lists per list round (shared list table)
 constexpr uint32_t kOutWords = kT + 8;           // staging window [t*kT-4, t*kT+kT+4)
 constexpr uint32_t kOutChunks = 1032;            // 16-B chunks incl. swizzle slack
 constexpr uint32_t kCCap = 1032;                 // staged control words (4 KiB + halo)
-constexpr uint32_t kDCap = 1280;                 // staged data vectors (20 KiB)
-constexpr uint32_t kECap = 4096;                 // staged exception bytes
+constexpr uint32_t kDCap = 1088;                 // staged data vectors (17 KiB)
+constexpr uint32_t kECap = 2048;                 // staged exception bytes
 constexpr uint32_t kResetWords = kOutWords / 32 + 2;
 
 // Look-back flags.
@@ -252,9 +254,11 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
     int64_t idx = base - lane;
     uint64_t s = (uint64_t)kFlagIncl << 32;
     if (idx >= 0) {
-      do {
+      s = ld_relaxed_u64(status + idx);
+      while ((s >> 32) == 0) {
+        __nanosleep(100);
         s = ld_relaxed_u64(status + idx);
-      } while ((s >> 32) == 0);
+      }
     }
     uint32_t flag = (uint32_t)(s >> 32), val = (uint32_t)s;
     uint32_t incl = __ballot_sync(0xffffffffu, flag == kFlagIncl);

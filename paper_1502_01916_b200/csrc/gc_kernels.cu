@@ -133,50 +133,97 @@ __device__ void validate_lists(const Dev& D, uint32_t tile, uint32_t* s_err) {
 // =====================================================================================
 // k_index (subsystem (a)): device-wide segmented scan over the control stream.
 // =====================================================================================
+constexpr uint32_t kLTA = kWA + 2;  // index-kernel list table entries (lists of one tile)
+
 template <class C>
 __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
-  __shared__ uint32_t s_w[kWA + 1];  // [0] = halo word (tile start - 1)
+  __shared__ uint32_t s_w[kWA + 1];     // [0] = halo word (tile start - 1)
+  __shared__ uint32_t s_cw[kLTA];       // first control word of each list, relative to w0
+  __shared__ uint32_t s_q[kLTA];        // quads of each list
+  __shared__ uint32_t s_jb[kLTA];       // first quad of the list holding a tile boundary
   __shared__ Seg3 s_scr[kWarps];
   __shared__ Seg3 s_prefix;
-  __shared__ uint32_t s_tile, s_err, s_first_reset;
+  __shared__ uint32_t s_tile, s_err, s_first_reset, s_nl;
+  __shared__ uint64_t s_la;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    s_tile = atomicAdd(&D.hdr->counter_a, 1u);
+    const uint32_t tile = atomicAdd(&D.hdr->counter_a, 1u);
+    s_tile = tile;
     s_err = 0;
+    const uint64_t w0 = (uint64_t)tile * kWA;
+    const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
+    // lists owning words [w0, w0+nw): la = owner of w0, lb = owner of the last word
+    uint64_t la = D.n_lists, lb = D.n_lists;
+    if (nw) {
+      la = find_list(D.ctrl_off, 0, D.n_lists + 1, 4 * w0);
+      lb = find_list(D.ctrl_off, la, D.n_lists + 1, 4 * (w0 + nw - 1));
+    }
+    s_la = la;
+    s_nl = la < D.n_lists ? (uint32_t)(mn64(lb, D.n_lists - 1) - la + 1) : 0u;
   }
   __syncthreads();
   const uint32_t tile = s_tile;
   validate_lists(D, tile, &s_err);
   const uint64_t w0 = (uint64_t)tile * kWA;
   const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
+  const uint64_t la = s_la;
+  const uint32_t nl = s_nl;
   for (uint32_t i = tid; i <= nw; i += kThreads) {
     int64_t gw = (int64_t)w0 - 1 + (int64_t)i;
     s_w[i] = (gw >= 0 && (uint64_t)gw < D.n_ctrl_words) ? D.ctrl_words[gw] : 0u;
+  }
+  for (uint32_t i = tid; i <= nl; i += kThreads) {
+    const uint64_t l = la + i;
+    s_cw[i] = (uint32_t)((D.ctrl_off[l] >> 2) - w0);  // may wrap for the first list
+    if (i < nl) {
+      const uint32_t n = D.list_n[l];
+      const uint64_t oo = D.out_off[l];
+      const uint64_t tb = (oo + kT - 1) / kT * kT;  // first tile boundary at or after oo
+      s_q[i] = (n + 3) >> 2;
+      s_jb[i] = tb < oo + n ? (uint32_t)((tb - oo) >> 2) : 0xFFFFFFFFu;
+    }
   }
   __syncthreads();
 
   const uint64_t my0 = w0 + (uint64_t)tid * kCA;
   const uint32_t myn = my0 < w0 + nw ? (uint32_t)mn64(kCA, w0 + nw - my0) : 0u;
-  ListCur L;
-  L.load(D, myn ? find_list(D.ctrl_off, 0, D.n_lists + 1, 4 * my0) : D.n_lists);
-  const ListCur L0 = L;
+  uint32_t li0 = 0;
+  if (myn && nl) {
+    const uint32_t key = (uint32_t)(my0 - w0);
+    uint32_t a = 0, b = nl;
+    while (b - a > 1) {
+      const uint32_t m = (a + b) >> 1;
+      if (s_cw[m] <= key) a = m;
+      else b = m;
+    }
+    li0 = a;
+  }
+  const uint32_t mynl = nl ? myn : 0u;
 
   // pass 1: per-word aggregates, segmented at list starts
   Seg3 agg{0, 0, 0, 0};
-  for (uint32_t k = 0; k < myn; k++) {
-    uint64_t w = my0 + k;
-    L.seek(D, w);
-    if (L.l >= D.n_lists) break;
-    WCtx c;
-    c.w = s_w[w - w0 + 1];
-    c.prev = s_w[w - w0];
-    c.widx = w - L.cw_lo;
-    c.Q = L.Q;
-    WAgg a = C::agg(c);
-    Seg3 v = c.widx == 0 ? Seg3{1u, a.q, L.dbase + a.d, L.ebase + a.e} : Seg3{0u, a.q, a.d, a.e};
-    agg = seg3_op(agg, v);
+  WAgg wa_[kCA];
+  uint32_t wli[kCA];
+  {
+    uint32_t li = li0;
+    for (uint32_t k = 0; k < kCA; k++) {
+      if (k >= mynl) break;
+      const uint32_t wr = (uint32_t)(my0 + k - w0);
+      while (li + 1 < nl && s_cw[li + 1] <= wr) li++;
+      wli[k] = li;
+      const uint32_t widx = wr - s_cw[li];
+      WCtx c{s_w[wr + 1], s_w[wr], widx, s_q[li]};
+      const WAgg a = C::agg(c);
+      wa_[k] = a;
+      if (widx == 0) {
+        const uint64_t l = la + li;
+        agg = Seg3{1u, a.q, D.data_off[l] * 32ull + a.d, (D.exc_off ? D.exc_off[l] : 0ull) + a.e};
+      } else {
+        agg = Seg3{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
+      }
+    }
   }
-  if (tid == 0) s_first_reset = (myn && L0.l < D.n_lists && my0 == L0.cw_lo) ? 1u : 0u;
+  if (tid == 0) s_first_reset = (mynl && s_cw[li0] == (uint32_t)(my0 - w0)) ? 1u : 0u;
   Seg3 total;
   Seg3 excl = block_excl_seg3(agg, s_scr, &total);
 
@@ -201,10 +248,11 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
       int64_t p = (int64_t)tile - 1;
       while (p >= 0) {
         TileA* t = D.tiles_a + p;
-        uint32_t f;
-        do {
+        uint32_t f = ld_relaxed_u32(&t->flag);
+        while (f == 0) {
+          __nanosleep(100);
           f = ld_relaxed_u32(&t->flag);
-        } while (f == 0);
+        }
         fence_gpu();
         if (f == kFlagIncl) {
           Seg3 v{1u, ld_relaxed_u32(&t->iq), ld_relaxed_u64(&t->id), ld_relaxed_u64(&t->ie)};
@@ -232,32 +280,37 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
   // last word, or a cheap test says it may be malformed), walk the groups: write the tile
   // Entries and check the groups' bounds
   Seg3 S = seg3_op(s_prefix, excl);
-  L = L0;
   uint32_t err = 0;
-  for (uint32_t k = 0; k < myn; k++) {
-    uint64_t w = my0 + k;
-    L.seek(D, w);
-    if (L.l >= D.n_lists) break;
-    WCtx c;
-    c.w = s_w[w - w0 + 1];
-    c.prev = s_w[w - w0];
-    c.widx = w - L.cw_lo;
-    c.Q = L.Q;
-    if (c.widx == 0) S = Seg3{1u, 0u, L.dbase, L.ebase};
+  for (uint32_t k = 0; k < kCA; k++) {
+    if (k >= mynl) break;
+    const uint64_t w = my0 + k;
+    const uint32_t wr = (uint32_t)(w - w0);
+    const uint32_t li = wli[k];
+    const uint32_t widx = wr - s_cw[li];
+    const uint32_t Q = s_q[li];
+    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q};
+    const WAgg a = wa_[k];
+    if (widx == 0) {
+      const uint64_t l = la + li;
+      S = Seg3{1u, 0u, D.data_off[l] * 32ull, D.exc_off ? D.exc_off[l] : 0ull};
+    }
     const Seg3 SW = S;
-    const WAgg a = C::agg(c);
     S.q += a.q;
     S.d += a.d;
     S.e += a.e;
-    const bool last = w + 1 == L.cw_hi;
-    if (last && (uint64_t)S.q < L.Q) err |= GC_DEV_TRUNCATED;  // control ends before Q quads
-    const uint64_t qa = SW.q, qb = mn64((uint64_t)SW.q + a.q, L.Q);
+    const bool last = li + 1 < nl ? s_cw[li + 1] == wr + 1
+                                  : (uint64_t)(D.ctrl_off[la + li + 1] >> 2) == w + 1;
+    if (last && S.q < Q) err |= GC_DEV_TRUNCATED;  // the control ends before Q quads
+    const uint32_t qa = SW.q, qb = min(SW.q + a.q, Q);
+    const uint32_t jb0 = s_jb[li];
     bool boundary = false;
-    if (qb > qa) {
-      const uint64_t lo_int = L.oo + 4 * qa, hi_int = L.oo + mn64(4 * qb, L.n);
-      boundary = ((lo_int + kT - 1) / kT) * kT < hi_int;
+    if (qb > qa && qb > jb0) {
+      const uint32_t kk = qa > jb0 ? (qa - jb0 + (kT / 4) - 1) / (kT / 4) : 0u;
+      boundary = jb0 + kk * (kT / 4) < qb;
     }
     if (!(boundary || last || C::suspect(c))) continue;
+    ListCur L;
+    L.load(D, la + li);
     C::walk(c, [&](const Grp& g) {
       uint64_t gq = (uint64_t)SW.q + g.q0;
       if (gq < L.Q && g.err) err |= g.err;
