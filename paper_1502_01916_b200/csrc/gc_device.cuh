@@ -15,20 +15,20 @@ constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kWA = 2048;
 constexpr uint32_t kCA = kWA / kThreads;
 
-// Decode kernel (output-space tiles): tile t owns the quadruples that contain the
-// output positions [t*kT, (t+1)*kT).
-constexpr uint32_t kT = 4096;
-constexpr uint32_t kCB = 2;                      // control words per thread per parse round
-constexpr uint32_t kRoundWords = kCB * kThreads; // 512
-constexpr uint32_t kQPT = 5;                     // quads per thread per unpack window
-constexpr uint32_t kRQ = kQPT * kThreads;        // quads per unpack window (1280)
-constexpr uint32_t kLT = 128;                    // lists per list round (shared list table)
+// Decode kernel (output-space warp-tiles): warp-tile t owns the quadruples that contain
+// the output positions [t*kT, (t+1)*kT).  One warp decodes one tile at a
+// time with warp-shuffle scans only; warps are persistent.
+constexpr uint32_t kT = 1024;
+constexpr uint32_t kCBW = 4;                     // control words per lane per parse round
+constexpr uint32_t kRoundWords = kCBW * 32;      // 128
+constexpr uint32_t kQPL = 9;                     // quads per lane per unpack window
+constexpr uint32_t kRQ = kQPL * 32;              // quads per unpack window (288)
+constexpr uint32_t kLT = 32;                     // lists per list round (per-warp list table)
 constexpr uint32_t kOutWords = kT + 8;           // staging window [t*kT-4, t*kT+kT+4)
-constexpr uint32_t kOutChunks = 1032;            // 16-B chunks incl. swizzle slack
-constexpr uint32_t kCCap = 1032;                 // staged control words (4 KiB + halo)
-constexpr uint32_t kDCap = 1088;                 // staged data vectors (17 KiB)
-constexpr uint32_t kECap = 2048;                 // staged exception bytes
-constexpr uint32_t kResetWords = kOutWords / 32 + 2;
+constexpr uint32_t kOutChunks = 264;             // 16-B chunks incl. swizzle slack
+constexpr uint32_t kCCap = 272;                  // staged control words (incl. halo)
+constexpr uint32_t kDCap = 288;                  // staged data vectors (4.5 KiB)
+constexpr uint32_t kECap = 768;                  // staged exception bytes
 
 // Look-back flags.
 constexpr uint32_t kFlagAgg = 1, kFlagIncl = 2;

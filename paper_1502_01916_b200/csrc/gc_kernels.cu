@@ -479,16 +479,27 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
     if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
   }
   if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
-  const uint32_t smem = DecodeSmem::bytes(C::kExc);
+  constexpr int kWPC = C::kExc ? 7 : 8;  // warps per CTA (shared memory: 2 CTAs per SM)
+  const uint32_t smem = kWPC * WarpSmem::bytes(C::kExc);
   static bool attr_set[2] = {false, false};
-  auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
+  static int n_sm = 0;
+  auto kern = dgaps ? k_decode<C, true, kWPC> : k_decode<C, false, kWPC>;
   if (!attr_set[dgaps]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return GC_ERR_CUDA;
     attr_set[dgaps] = true;
   }
-  kern<<<(unsigned)D.n_tiles_b, kThreads, smem, st>>>(D, out);
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  // persistent: enough CTAs to fill every SM, never more warps than tiles
+  const uint64_t want = (D.n_tiles_b + kWPC - 1) / kWPC;
+  const unsigned grid = (unsigned)mn64(want, (uint64_t)n_sm * 2);
+  kern<<<grid, 32 * kWPC, smem, st>>>(D, out);
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
 
