@@ -39,6 +39,7 @@ struct WCtx {
   uint32_t prev;   // previous control word of the same list (valid iff widx > 0)
   uint64_t widx;   // word index within the list's control area
   uint64_t Q;      // quads of the list
+  uint32_t part;   // which kParts-th of the word (codecs with kParts > 1)
 };
 
 struct WAgg {
@@ -70,6 +71,7 @@ __device__ __forceinline__ uint32_t gs_bw(uint32_t s) {
 
 struct CodecGS {
   static constexpr bool kExc = false;
+  static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;   // a group may hold several quads
   static constexpr bool kVectorGroups = true;
@@ -113,6 +115,9 @@ struct CodecGscB {
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
   static constexpr int kFields = CG == 1 ? 6 : (CG == 8 ? 16 : 8);
+  // a word is parsed as kParts units of kFields/kParts fields (balances the work per lane)
+  static constexpr int kParts = CG == 8 ? 4 : 2;
+  static constexpr int kPF = kFields / kParts;
   __device__ static __forceinline__ uint32_t field(uint32_t w, int k) {
     if (CG == 1) return (w >> (16 * (k / 3) + 5 * (k % 3))) & 31u;
     if (CG == 2) return (w >> (4 * k)) & 15u;
@@ -122,20 +127,20 @@ struct CodecGscB {
   __device__ static WAgg agg(const WCtx& c) {
     uint32_t d = 0;
 #pragma unroll
-    for (int k = 0; k < kFields; k++) d += CG * (field(c.w, k) + 1);  // Eq. (2)
-    return WAgg{(uint32_t)kFields, d, 0u};
+    for (int k = 0; k < kPF; k++) d += CG * (field(c.w, c.part * kPF + k) + 1);  // Eq. (2)
+    return WAgg{(uint32_t)kPF, d, 0u};
   }
   __device__ static bool suspect(const WCtx&) { return false; }  // every field value is valid
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
     int32_t d = 0;
 #pragma unroll
-    for (int k = 0; k < kFields; k++) {
+    for (int k = 0; k < kPF; k++) {
       Grp g = grp0();
       g.q0 = k;
       g.nq = 1;
       g.d0 = d;
-      g.bw = CG * (field(c.w, k) + 1);  // BW = CG*(LD+1)
+      g.bw = CG * (field(c.w, c.part * kPF + k) + 1);  // BW = CG*(LD+1)
       g.dlen = g.bw;
       f(g);
       d += (int32_t)g.bw;
@@ -151,6 +156,7 @@ struct CodecGscB {
 template <int CG>
 struct CodecGscCU {
   static constexpr bool kExc = false;
+  static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = true;
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
@@ -211,6 +217,7 @@ struct CodecGscCU {
 template <int CG>
 struct CodecGscIU {
   static constexpr bool kExc = false;
+  static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
@@ -279,6 +286,7 @@ struct CodecGscIU {
 // Each frame starts a fresh 128-bit vector: ceil(L*bw/32) vectors.
 struct CodecAFOR {
   static constexpr bool kExc = false;
+  static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
@@ -326,6 +334,7 @@ struct CodecAFOR {
 template <int F>
 struct CodecPFD {
   static constexpr bool kExc = true;
+  static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
@@ -365,5 +374,40 @@ struct CodecPFD {
     f(g);
   }
 };
+
+// Whole-word helpers over a codec's kParts units (the index kernel parses whole words).
+template <class C>
+__device__ __forceinline__ WAgg word_agg(WCtx c) {
+  WAgg t{0, 0, 0};
+#pragma unroll
+  for (int p = 0; p < C::kParts; p++) {
+    c.part = p;
+    const WAgg a = C::agg(c);
+    t.q += a.q;
+    t.d += a.d;
+    t.e += a.e;
+  }
+  return t;
+}
+template <class C, class F>
+__device__ __forceinline__ void word_walk(WCtx c, F&& f) {
+  uint32_t q = 0, d = 0, e = 0;
+#pragma unroll
+  for (int p = 0; p < C::kParts; p++) {
+    c.part = p;
+    C::walk(c, [&](Grp g) {
+      g.q0 += q;
+      g.d0 += (int32_t)d;
+      g.e0 += e;
+      f(g);
+    });
+    if (C::kParts > 1) {
+      const WAgg a = C::agg(c);
+      q += a.q;
+      d += a.d;
+      e += a.e;
+    }
+  }
+}
 
 }  // namespace gcd

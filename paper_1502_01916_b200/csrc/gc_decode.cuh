@@ -254,12 +254,15 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
 
       for (uint32_t u = 0; u < K; u += kRQ) {
         St carry = carry0;
-        for (uint64_t r0 = rw0; r0 < rw1; r0 += kRoundWords) {
+        // control units (a word, or a kParts-th of one) in rounds of 32 x kCBW
+        constexpr uint32_t P = C::kParts;
+        const uint64_t ru0 = rw0 * P, ru1 = rw1 * P;
+        for (uint64_t r0 = ru0; r0 < ru1; r0 += kRoundWords) {
           const uint64_t my0 = r0 + (uint64_t)lane * kCBW;
-          const uint32_t myn = my0 < rw1 ? (uint32_t)mn64(kCBW, rw1 - my0) : 0u;
+          const uint32_t myn = my0 < ru1 ? (uint32_t)mn64(kCBW, ru1 - my0) : 0u;
           uint32_t li = 0;
           if (myn) {  // the last table entry whose first word is <= my first word
-            const uint32_t key = (uint32_t)(my0 - cbase);
+            const uint32_t key = (uint32_t)(my0 / P - cbase);
             uint32_t a = 0, b = cnt;
             while (b - a > 1) {
               const uint32_t m = (a + b) >> 1;
@@ -272,7 +275,9 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
           St agg{0, 0, 0, 0};
 #pragma unroll
           for (uint32_t k = 0; k < kCBW; k++) {
-            const uint64_t w = my0 + k;
+            const uint64_t un = my0 + k;
+            const uint64_t w = un / P;
+            const uint32_t part = (uint32_t)(un % P);
             const uint32_t wr = (uint32_t)(w - cbase);
             wv[k] = pv[k] = wl[k] = 0;
             if (k < myn) {
@@ -281,10 +286,11 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
               wv[k] = wr < ncw ? cwp[wr] : 0u;
               pv[k] = (C::kNeedsPrev && wr >= 1 && wr - 1 < ncw) ? cwp[wr - 1] : 0u;
               const uint32_t widx = wr - lt_cw[li];
-              const WCtx c{wv[k], pv[k], widx, lt_q[li]};
+              const WCtx c{wv[k], pv[k], widx, lt_q[li], part};
               const WAgg a = C::agg(c);
-              agg = (widx == 0 && w != wa) ? St{1u, a.q, lt_db[li] + a.d, lt_eb[li] + a.e}
-                                           : St{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
+              agg = (widx == 0 && part == 0 && w != wa)
+                        ? St{1u, a.q, lt_db[li] + a.d, lt_eb[li] + a.e}
+                        : St{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
             }
           }
           St rtot;
@@ -295,12 +301,14 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
 #pragma unroll
           for (uint32_t k = 0; k < kCBW; k++) {
             if (k >= myn) break;
-            const uint64_t w = my0 + k;
+            const uint64_t un = my0 + k;
+            const uint64_t w = un / P;
+            const uint32_t part = (uint32_t)(un % P);
             const uint32_t wr = (uint32_t)(w - cbase);
             const uint32_t i = wl[k];
             const uint32_t widx = wr - lt_cw[i];
-            const WCtx c{wv[k], pv[k], widx, lt_q[i]};
-            if (widx == 0 && w != wa) S = St{1u, 0u, lt_db[i], lt_eb[i]};
+            const WCtx c{wv[k], pv[k], widx, lt_q[i], part};
+            if (widx == 0 && part == 0 && w != wa) S = St{1u, 0u, lt_db[i], lt_eb[i]};
             const WAgg a = C::agg(c);
             const uint32_t klo = lt_klo[i], kend = lt_kend[i];
             const uint32_t qa = max(S.q, klo), qb = min(S.q + a.q, kend);
@@ -471,47 +479,47 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
     if (!waited) mbar_wait(bar, phase);
     phase ^= 1u;
 
-    // ---------------------------------------------------------------- look-back
-    uint32_t cin = 0;
+    // ---------------------------------------------------------------- look-back + store
+    // publish the tile aggregate, store every chunk that needs no carry, then look back
+    // and store the tile's first list segment (before its first list start)
+    const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
+    const int64_t cb = base_int / 4;
+    auto store_chunk = [&](int64_t c, uint32_t cin, uint32_t r0) {
+      const uint32_t lc = (uint32_t)(c - cb);
+      uint4 v = s_out4[sw_chunk(lc)];
+      if (cin) {
+        const uint32_t p = 4 * lc;
+        if (p < r0) v.x += cin;
+        if (p + 1 < r0) v.y += cin;
+        if (p + 2 < r0) v.z += cin;
+        if (p + 3 < r0) v.w += cin;
+      }
+      const int64_t g = 4 * c;
+      if (g >= out_lo && g + 4 <= out_hi) {
+        __stcs(reinterpret_cast<uint4*>(out + g), v);
+      } else {
+        const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
+        for (int k = 0; k < 4; k++)
+          if (g + k >= out_lo && g + k < out_hi) out[g + k] = a4[k];
+      }
+    };
+    const bool need_carry = DGAPS && j0 > 0;  // the tile's first quad continues a list
     if (DGAPS) {
       reset0 = __reduce_min_sync(0xffffffffu, reset0);
-      const bool need_carry = j0 > 0;  // the tile's first quad continues a list
       if (lane == 0)
         st_relaxed_u64(D.tiles_b + tile,
                        ((uint64_t)((rcarry.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) |
                            rcarry.v);
-      if (need_carry) {
-        cin = lookback_u32(D.tiles_b, tile);
-        if (lane == 0 && !rcarry.f)
-          st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + rcarry.v));
-      }
     }
-
-    // ---------------------------------------------------------------- coalesced store
-    // 128-bit stores of [out_lo, out_hi); the tile's first list segment (before its first
-    // list start) gets the carry from the look-back
-    {
-      const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
-      const int64_t cb = base_int / 4;
-      for (int64_t c = c_lo + lane; c < c_hi; c += 32) {
-        const uint32_t lc = (uint32_t)(c - cb);
-        uint4 v = s_out4[sw_chunk(lc)];
-        if (DGAPS && cin) {
-          const uint32_t p = 4 * lc;
-          if (p < reset0) v.x += cin;
-          if (p + 1 < reset0) v.y += cin;
-          if (p + 2 < reset0) v.z += cin;
-          if (p + 3 < reset0) v.w += cin;
-        }
-        const int64_t g = 4 * c;
-        if (g >= out_lo && g + 4 <= out_hi) {
-          __stcs(reinterpret_cast<uint4*>(out + g), v);
-        } else {
-          const uint32_t a[4] = {v.x, v.y, v.z, v.w};
-          for (int k = 0; k < 4; k++)
-            if (g + k >= out_lo && g + k < out_hi) out[g + k] = a[k];
-        }
-      }
+    // chunks whose every int lies at or after the first list start: final already
+    const int64_t c_mid =
+        need_carry ? smin64(c_hi, smax64(c_lo, (base_int + (int64_t)reset0 + 3) >> 2)) : c_lo;
+    for (int64_t c = c_mid + lane; c < c_hi; c += 32) store_chunk(c, 0u, 0u);
+    if (need_carry) {
+      const uint32_t cin = lookback_u32(D.tiles_b, tile);
+      if (lane == 0 && !rcarry.f)
+        st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + rcarry.v));
+      for (int64_t c = c_lo + lane; c < c_mid; c += 32) store_chunk(c, cin, reset0);
     }
     __syncwarp();
   }

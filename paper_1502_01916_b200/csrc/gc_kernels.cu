@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
       while (li + 1 < nl && s_cw[li + 1] <= wr) li++;
       wli[k] = li;
       const uint32_t widx = wr - s_cw[li];
-      WCtx c{s_w[wr + 1], s_w[wr], widx, s_q[li]};
-      const WAgg a = C::agg(c);
+      WCtx c{s_w[wr + 1], s_w[wr], widx, s_q[li], 0u};
+      const WAgg a = word_agg<C>(c);
       wa_[k] = a;
       if (widx == 0) {
         const uint64_t l = la + li;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
     const uint32_t li = wli[k];
     const uint32_t widx = wr - s_cw[li];
     const uint32_t Q = s_q[li];
-    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q};
+    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q, 0u};
     const WAgg a = wa_[k];
     if (widx == 0) {
       const uint64_t l = la + li;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
     if (!(boundary || last || C::suspect(c))) continue;
     ListCur L;
     L.load(D, la + li);
-    C::walk(c, [&](const Grp& g) {
+    word_walk<C>(c, [&](const Grp& g) {
       uint64_t gq = (uint64_t)SW.q + g.q0;
       if (gq < L.Q && g.err) err |= g.err;
       if (gq >= L.Q || g.nq == 0) return;
