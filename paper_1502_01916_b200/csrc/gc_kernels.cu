@@ -143,13 +143,17 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
   __shared__ uint32_t s_jb[kLTA];       // first quad of the list holding a tile boundary
   __shared__ Seg3 s_scr[kWarps];
   __shared__ Seg3 s_prefix;
-  __shared__ uint32_t s_tile, s_err, s_first_reset, s_nl;
+  __shared__ uint32_t s_tile, s_err, s_first_reset, s_nl, s_nq;
   __shared__ uint64_t s_la;
+  constexpr uint32_t kQueue = 384;  // words needing a group walk (list ends, tile boundaries)
+  __shared__ uint32_t s_qw[kQueue], s_qq[kQueue];
+  __shared__ uint64_t s_qd[kQueue], s_qe[C::kExc ? kQueue : 1];
   const int tid = threadIdx.x;
   if (tid == 0) {
     const uint32_t tile = atomicAdd(&D.hdr->counter_a, 1u);
     s_tile = tile;
     s_err = 0;
+    s_nq = 0;
     const uint64_t w0 = (uint64_t)tile * kWA;
     const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
     // lists owning words [w0, w0+nw): la = owner of w0, lb = owner of the last word
@@ -279,36 +283,8 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
   // pass 2: per word, only where needed (a tile boundary falls in it, it is the list's
   // last word, or a cheap test says it may be malformed), walk the groups: write the tile
   // Entries and check the groups' bounds
-  Seg3 S = seg3_op(s_prefix, excl);
   uint32_t err = 0;
-  for (uint32_t k = 0; k < kCA; k++) {
-    if (k >= mynl) break;
-    const uint64_t w = my0 + k;
-    const uint32_t wr = (uint32_t)(w - w0);
-    const uint32_t li = wli[k];
-    const uint32_t widx = wr - s_cw[li];
-    const uint32_t Q = s_q[li];
-    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q, 0u};
-    const WAgg a = wa_[k];
-    if (widx == 0) {
-      const uint64_t l = la + li;
-      S = Seg3{1u, 0u, D.data_off[l] * 32ull, D.exc_off ? D.exc_off[l] : 0ull};
-    }
-    const Seg3 SW = S;
-    S.q += a.q;
-    S.d += a.d;
-    S.e += a.e;
-    const bool last = li + 1 < nl ? s_cw[li + 1] == wr + 1
-                                  : (uint64_t)(D.ctrl_off[la + li + 1] >> 2) == w + 1;
-    if (last && S.q < Q) err |= GC_DEV_TRUNCATED;  // the control ends before Q quads
-    const uint32_t qa = SW.q, qb = min(SW.q + a.q, Q);
-    const uint32_t jb0 = s_jb[li];
-    bool boundary = false;
-    if (qb > qa && qb > jb0) {
-      const uint32_t kk = qa > jb0 ? (qa - jb0 + (kT / 4) - 1) / (kT / 4) : 0u;
-      boundary = jb0 + kk * (kT / 4) < qb;
-    }
-    if (!(boundary || last || C::suspect(c))) continue;
+  auto walk_word = [&](uint64_t w, uint32_t li, const WCtx& c, const Seg3& SW) {
     ListCur L;
     L.load(D, la + li);
     word_walk<C>(c, [&](const Grp& g) {
@@ -346,6 +322,54 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
         D.entries[t] = e;
       }
     });
+  };
+  Seg3 S = seg3_op(s_prefix, excl);
+  for (uint32_t k = 0; k < kCA; k++) {
+    if (k >= mynl) break;
+    const uint64_t w = my0 + k;
+    const uint32_t wr = (uint32_t)(w - w0);
+    const uint32_t li = wli[k];
+    const uint32_t widx = wr - s_cw[li];
+    const uint32_t Q = s_q[li];
+    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q, 0u};
+    const WAgg a = wa_[k];
+    if (widx == 0) {
+      const uint64_t l = la + li;
+      S = Seg3{1u, 0u, D.data_off[l] * 32ull, D.exc_off ? D.exc_off[l] : 0ull};
+    }
+    const Seg3 SW = S;
+    S.q += a.q;
+    S.d += a.d;
+    S.e += a.e;
+    const bool last = li + 1 < nl ? s_cw[li + 1] == wr + 1
+                                  : (uint64_t)(D.ctrl_off[la + li + 1] >> 2) == w + 1;
+    if (last && S.q < Q) err |= GC_DEV_TRUNCATED;  // the control ends before Q quads
+    const uint32_t qa = SW.q, qb = min(SW.q + a.q, Q);
+    const uint32_t jb0 = s_jb[li];
+    bool boundary = false;
+    if (qb > qa && qb > jb0) {
+      const uint32_t kk = qa > jb0 ? (qa - jb0 + (kT / 4) - 1) / (kT / 4) : 0u;
+      boundary = jb0 + kk * (kT / 4) < qb;
+    }
+    if (!(boundary || last || C::suspect(c))) continue;
+    // compact the words that need a group walk into a queue so the walks run lane-dense
+    const uint32_t slot = atomicAdd(&s_nq, 1u);
+    if (slot < kQueue) {
+      s_qw[slot] = wr | (li << 16);
+      s_qq[slot] = SW.q;
+      s_qd[slot] = SW.d;
+      if (C::kExc) s_qe[slot] = SW.e;
+    } else {
+      walk_word(w, li, c, SW);  // queue full: walk in place
+    }
+  }
+  __syncthreads();
+  const uint32_t nq = min(s_nq, kQueue);
+  for (uint32_t i = tid; i < nq; i += kThreads) {
+    const uint32_t wr = s_qw[i] & 0xFFFFu, li = s_qw[i] >> 16;
+    const Seg3 SW{0u, s_qq[i], s_qd[i], C::kExc ? s_qe[i] : 0ull};
+    const WCtx c{s_w[wr + 1], s_w[wr], wr - s_cw[li], s_q[li], 0u};
+    walk_word(w0 + wr, li, c, SW);
   }
   report(&s_err, err);
   __syncthreads();
