@@ -131,6 +131,18 @@ struct CodecGscB {
     return WAgg{(uint32_t)kPF, d, 0u};
   }
   __device__ static bool suspect(const WCtx&) { return false; }  // every field value is valid
+  // emit(j, pos, bw) for the quads j in [qa, qb) of this unit (q, d: the unit's prefix)
+  template <class F>
+  __device__ static __forceinline__ void emit(const WCtx& c, uint32_t q, uint32_t d, uint32_t qa,
+                                              uint32_t qb, F&& f) {
+#pragma unroll
+    for (int k = 0; k < kPF; k++) {
+      const uint32_t bw = CG * (field(c.w, c.part * kPF + k) + 1);
+      const uint32_t j = q + k;
+      if (j >= qa && j < qb) f(j, d, bw);
+      d += bw;
+    }
+  }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
     int32_t d = 0;
@@ -175,6 +187,24 @@ struct CodecGscCU {
     }
     if (have < 32u / CG) y &= y >> (32u / CG - have);
     return (uint32_t)y != 0;
+  }
+  template <class F>
+  __device__ static __forceinline__ void emit(const WCtx& c, uint32_t q, uint32_t d, uint32_t qa,
+                                              uint32_t qb, F&& f) {
+    int32_t start = 0;
+    if (c.widx > 0) {
+      const uint32_t mp = ~__byte_perm(c.prev, 0, 0x0123);
+      start = mp ? -(int32_t)(__ffs(mp) - 1) : -32;
+    }
+    uint32_t m = ~__byte_perm(c.w, 0, 0x0123);
+    uint32_t j = q;
+    while (m && j < qb) {
+      const int32_t z = (int32_t)__clz(m);
+      if (j >= qa) f(j, d + (uint32_t)(CG * start), min(32u, (uint32_t)(CG * (z - start + 1))));
+      start = z + 1;
+      m ^= 0x80000000u >> z;
+      j++;
+    }
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
@@ -242,6 +272,24 @@ struct CodecGscIU {
       if (y & 0xFFu) return true;
     }
     return false;
+  }
+  template <class F>
+  __device__ static __forceinline__ void emit(const WCtx& c, uint32_t q, uint32_t d, uint32_t qa,
+                                              uint32_t qb, F&& f) {
+    uint32_t j = q;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t mm = (~(c.w >> (8 * i)) & 0xFFu) << 24;
+      uint32_t start = 0;
+      while (mm && j < qb) {
+        const uint32_t z = __clz(mm);
+        if (j >= qa) f(j, d + CG * start, min(32u, CG * (z - start + 1)));
+        start = z + 1;
+        mm ^= 0x80000000u >> z;
+        j++;
+      }
+      d += CG * start;  // used bits of the byte (the trailing 1s are padding)
+    }
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {

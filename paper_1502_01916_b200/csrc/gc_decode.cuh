@@ -123,12 +123,52 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
   uint32_t phase = 0;
   uint32_t err = 0;
 
+  // 128-bit store of staging chunk c (the 16-B output block 4c..4c+3 clipped to [lo, hi));
+  // ints before staging index r0 get the look-back carry cin
+  auto store_chunk = [&](int64_t c, int64_t cb, int64_t lo, int64_t hi, uint32_t cin, uint32_t r0) {
+    const uint32_t lc = (uint32_t)(c - cb);
+    uint4 v = s_out4[sw_chunk(lc)];
+    if (cin) {
+      const uint32_t p = 4 * lc;
+      if (p < r0) v.x += cin;
+      if (p + 1 < r0) v.y += cin;
+      if (p + 2 < r0) v.z += cin;
+      if (p + 3 < r0) v.w += cin;
+    }
+    const int64_t g = 4 * c;
+    if (g >= lo && g + 4 <= hi) {
+      __stcs(reinterpret_cast<uint4*>(out + g), v);
+    } else {
+      const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
+      for (int k = 0; k < 4; k++)
+        if (g + k >= lo && g + k < hi) out[g + k] = a4[k];
+    }
+  };
+  // A tile whose first list segment needs the carry of earlier tiles is finished only after
+  // this warp has claimed and set up its next tile, so the look-back wait overlaps that
+  // tile's bulk copies (its staging window is not touched before then).
+  bool pd_on = false;
+  uint32_t pd_tile = 0, pd_reset0 = 0, pd_f = 0, pd_v = 0;
+  int64_t pd_lo = 0, pd_hi = 0, pd_clo = 0, pd_cmid = 0, pd_cb = 0;
+  auto finish_pending = [&]() {
+    if (!pd_on) return;
+    const uint32_t cin = lookback_u32(D.tiles_b, pd_tile);
+    if (lane == 0 && !pd_f)
+      st_relaxed_u64(D.tiles_b + pd_tile, ((uint64_t)kFlagIncl << 32) | (cin + pd_v));
+    for (int64_t c = pd_clo + lane; c < pd_cmid; c += 32) store_chunk(c, pd_cb, pd_lo, pd_hi, cin, pd_reset0);
+    pd_on = false;
+    __syncwarp();
+  };
+
   while (true) {
     // ---------------------------------------------------------------- claim a tile
     uint32_t tile = 0;
     if (lane == 0) tile = atomicAdd(&D.hdr->counter_b, 1u);
     tile = __shfl_sync(0xffffffffu, tile, 0);
-    if (tile >= D.n_tiles_b) break;
+    if (tile >= D.n_tiles_b) {
+      finish_pending();
+      break;
+    }
     // the two boundary Entries (80 B each) -> shared, 20 lanes x 2 words
     {
       const uint32_t* e0p = reinterpret_cast<const uint32_t*>(D.entries + tile);
@@ -186,6 +226,7 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
       if (data_staged && vb > va) bulk_g2s(s_data, D.data + va, (uint32_t)(vb - va) * 16, bar);
       if (C::kExc && exc_staged && eb > ea) bulk_g2s(s_exc, D.exc + ea, (uint32_t)(eb - ea), bar);
     }
+    finish_pending();  // the previous tile's look-back, now that this tile's copies are in flight
     const uint32_t ncw = (uint32_t)(cstop - cbase);
     const uint32_t* cwp = ctrl_staged ? s_ctrl : D.ctrl_words + cbase;  // word w at cwp[w-cbase]
     const uint4* dptr = data_staged ? s_data : D.data + va;
@@ -313,7 +354,21 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
             const uint32_t klo = lt_klo[i], kend = lt_kend[i];
             const uint32_t qa = max(S.q, klo), qb = min(S.q + a.q, kend);
             const uint32_t x0 = lt_lb[i] + (qa - klo);  // local index of quad qa
-            if (qb > qa && x0 < u + kRQ && x0 + (qb - qa) > u) {
+            if (!(qb > qa && x0 < u + kRQ && x0 + (qb - qa) > u)) {
+            } else if constexpr (!C::kMultiQuad) {
+              // one quad per group: tight codec loop straight into the descriptors
+              const uint32_t ja = qa + (u > x0 ? u - x0 : 0u);
+              const uint32_t jb = min(qb, qa + (u + kRQ - x0));
+              const uint32_t n = lt_n[i], oref = lt_oref[i];
+              const uint32_t lbase = x0 - qa - u;  // descriptor slot of quad j = lbase + j
+              C::emit(c, S.q, S.d, ja, jb, [&](uint32_t j, uint32_t pos, uint32_t bw) {
+                const uint32_t op = oref + 4u * j;
+                const uint32_t cq = min(4u, n - 4u * j);
+                const uint32_t rst = j == 0 ? 1u : 0u;
+                s_desc[lbase + j] = make_uint2(pos, bw | (op << 6) | ((cq - 1) << 19) | (rst << 21));
+                if (DGAPS && rst) reset0 = min(reset0, op);
+              });
+            } else {
               const St SW = S;
               const uint32_t n = lt_n[i], oref = lt_oref[i], Qi = lt_q[i];
               C::walk(c, [&](const Grp& g) {
@@ -388,7 +443,7 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
           if (qi < nr) {
             const uint2 dsc = s_desc[qi];
             const uint32_t bw = dsc.y & 63u;
-            op = (dsc.y >> 6) & 0x1FFFu;
+            op = min((dsc.y >> 6) & 0x1FFFu, kOutWords - 4);
             c = ((dsc.y >> 19) & 3u) + 1u;
             rst = (dsc.y >> 21) & 1u;
             const uint32_t m = dsc.x >> 5, off = dsc.x & 31u;
@@ -479,30 +534,11 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
     if (!waited) mbar_wait(bar, phase);
     phase ^= 1u;
 
-    // ---------------------------------------------------------------- look-back + store
-    // publish the tile aggregate, store every chunk that needs no carry, then look back
-    // and store the tile's first list segment (before its first list start)
+    // ---------------------------------------------------------------- publish + store
+    // publish the tile aggregate and store every chunk that needs no carry; the first list
+    // segment (before the tile's first list start) waits for the look-back
     const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
     const int64_t cb = base_int / 4;
-    auto store_chunk = [&](int64_t c, uint32_t cin, uint32_t r0) {
-      const uint32_t lc = (uint32_t)(c - cb);
-      uint4 v = s_out4[sw_chunk(lc)];
-      if (cin) {
-        const uint32_t p = 4 * lc;
-        if (p < r0) v.x += cin;
-        if (p + 1 < r0) v.y += cin;
-        if (p + 2 < r0) v.z += cin;
-        if (p + 3 < r0) v.w += cin;
-      }
-      const int64_t g = 4 * c;
-      if (g >= out_lo && g + 4 <= out_hi) {
-        __stcs(reinterpret_cast<uint4*>(out + g), v);
-      } else {
-        const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
-        for (int k = 0; k < 4; k++)
-          if (g + k >= out_lo && g + k < out_hi) out[g + k] = a4[k];
-      }
-    };
     const bool need_carry = DGAPS && j0 > 0;  // the tile's first quad continues a list
     if (DGAPS) {
       reset0 = __reduce_min_sync(0xffffffffu, reset0);
@@ -511,15 +547,20 @@ __global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uin
                        ((uint64_t)((rcarry.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) |
                            rcarry.v);
     }
-    // chunks whose every int lies at or after the first list start: final already
     const int64_t c_mid =
         need_carry ? smin64(c_hi, smax64(c_lo, (base_int + (int64_t)reset0 + 3) >> 2)) : c_lo;
-    for (int64_t c = c_mid + lane; c < c_hi; c += 32) store_chunk(c, 0u, 0u);
+    for (int64_t c = c_mid + lane; c < c_hi; c += 32) store_chunk(c, cb, out_lo, out_hi, 0u, 0u);
     if (need_carry) {
-      const uint32_t cin = lookback_u32(D.tiles_b, tile);
-      if (lane == 0 && !rcarry.f)
-        st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + rcarry.v));
-      for (int64_t c = c_lo + lane; c < c_mid; c += 32) store_chunk(c, cin, reset0);
+      pd_on = true;
+      pd_tile = tile;
+      pd_reset0 = reset0;
+      pd_f = rcarry.f;
+      pd_v = rcarry.v;
+      pd_lo = out_lo;
+      pd_hi = out_hi;
+      pd_clo = c_lo;
+      pd_cmid = c_mid;
+      pd_cb = cb;
     }
     __syncwarp();
   }
