@@ -245,33 +245,40 @@ __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* tot
 // ---------------------------------------------------------------- decoupled look-back
 // d-gap carry: one 64-bit word per tile, (flag << 32) | value.  Called by one full
 // warp; returns the sum of the aggregates of the tiles before `tile` back to (and
-// including) the nearest tile that published an inclusive prefix.
+// including) the nearest tile that published an inclusive prefix.  Lane i watches tile
+// base-i; a window is usable as soon as every lane up to the nearest inclusive one has
+// published (the older tiles of the window are not waited for).
 __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile) {
-  const int lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31;
   uint32_t acc = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
-    int64_t idx = base - lane;
-    uint64_t s = (uint64_t)kFlagIncl << 32;
-    if (idx >= 0) {
-      s = ld_relaxed_u64(status + idx);
-      while ((s >> 32) == 0) {
-        __nanosleep(100);
+    const int64_t idx = base - (int64_t)lane;
+    uint64_t s = (uint64_t)kFlagIncl << 32;  // before tile 0: an empty inclusive prefix
+    if (idx >= 0) s = ld_relaxed_u64(status + idx);
+    while (true) {
+      const uint32_t flag = (uint32_t)(s >> 32);
+      const uint32_t valid = __ballot_sync(0xffffffffu, flag != 0);
+      const uint32_t incl = __ballot_sync(0xffffffffu, flag == kFlagIncl);
+      const uint32_t first = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
+      const uint32_t need = first == 31u ? 0xffffffffu : ((2u << first) - 1u);
+      if ((valid & need) == need) break;
+      if (!(valid & (1u << lane)) && (need & (1u << lane))) {
+        __nanosleep(32);
         s = ld_relaxed_u64(status + idx);
       }
     }
-    uint32_t flag = (uint32_t)(s >> 32), val = (uint32_t)s;
-    uint32_t incl = __ballot_sync(0xffffffffu, flag == kFlagIncl);
+    const uint32_t flag = (uint32_t)(s >> 32);
+    const uint32_t incl = __ballot_sync(0xffffffffu, flag == kFlagIncl);
+    uint32_t mine = (uint32_t)s;
     if (incl) {
-      int first = __ffs(incl) - 1;  // nearest inclusive predecessor
-      uint32_t mine = lane <= first ? val : 0u;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-      return acc + mine;
+      const uint32_t first = (uint32_t)(__ffs(incl) - 1);  // nearest inclusive predecessor
+      if (lane > first) mine = 0;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-    acc += val;
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    acc += mine;
+    if (incl) return acc;
     base -= 32;
   }
 }
