@@ -32,6 +32,8 @@ struct Grp {
   uint32_t cnt;   // PFD exception count
   uint32_t wb;    // PFD exception value bytes (1/2/4)
   uint32_t err;   // GC_DEV_* bits, reported only if the group starts before the list end
+  uint32_t t0;    // PFD: first quad of the group within its frame
+  uint32_t fq;    // PFD: quads of the frame (the list's tail frame may be short)
 };
 
 struct WCtx {
@@ -49,7 +51,7 @@ struct WAgg {
 __device__ __forceinline__ Grp grp0() {
   Grp g;
   g.q0 = 0; g.nq = 0; g.d0 = 0; g.dlen = 0; g.bw = 1; g.step = 0;
-  g.e0 = 0; g.elen = 0; g.cnt = 0; g.wb = 0; g.err = 0;
+  g.e0 = 0; g.elen = 0; g.cnt = 0; g.wb = 0; g.err = 0; g.t0 = 0; g.fq = 0;
   return g;
 }
 
@@ -71,15 +73,16 @@ __device__ __forceinline__ uint32_t gs_bw(uint32_t s) {
 
 struct CodecGS {
   static constexpr bool kExc = false;
-  static constexpr int kParts = 1;
+  static constexpr uint64_t kBackBits = 0;
+  static constexpr int kParts = 2;           // a parse unit = 4 selectors (half a word)
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;   // a group may hold several quads
   static constexpr bool kVectorGroups = true;
   __device__ static WAgg agg(const WCtx& c) {
     uint32_t q = 0;
 #pragma unroll
-    for (int k = 0; k < 8; k++) q += gs_num((c.w >> (4 * k)) & 15u);  // low nibble first (A6)
-    return WAgg{q, 8u * 32u, 0u};
+    for (int k = 0; k < 4; k++) q += gs_num((c.w >> (16 * c.part + 4 * k)) & 15u);  // low nibble first (A6)
+    return WAgg{q, 4u * 32u, 0u};
   }
   // may the word hold a malformed group?  (a nibble > 9: bit 3 and bit 2 or 1)
   __device__ static bool suspect(const WCtx& c) {
@@ -89,8 +92,8 @@ struct CodecGS {
   __device__ static void walk(const WCtx& c, F&& f) {
     uint32_t q = 0;
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      uint32_t s = (c.w >> (4 * k)) & 15u;
+    for (int k = 0; k < 4; k++) {
+      uint32_t s = (c.w >> (16 * c.part + 4 * k)) & 15u;
       Grp g = grp0();
       g.q0 = q;
       g.nq = gs_num(s);
@@ -111,6 +114,7 @@ struct CodecGS {
 template <int CG>
 struct CodecGscB {
   static constexpr bool kExc = false;
+  static constexpr uint64_t kBackBits = 0;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
@@ -168,6 +172,7 @@ struct CodecGscB {
 template <int CG>
 struct CodecGscCU {
   static constexpr bool kExc = false;
+  static constexpr uint64_t kBackBits = 32 * CG;  // a code may start in the previous word
   static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = true;
   static constexpr bool kMultiQuad = false;
@@ -247,6 +252,7 @@ struct CodecGscCU {
 template <int CG>
 struct CodecGscIU {
   static constexpr bool kExc = false;
+  static constexpr uint64_t kBackBits = 0;
   static constexpr int kParts = 1;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = false;
@@ -334,44 +340,32 @@ struct CodecGscIU {
 // Each frame starts a fresh 128-bit vector: ceil(L*bw/32) vectors.
 struct CodecAFOR {
   static constexpr bool kExc = false;
-  static constexpr int kParts = 1;
+  static constexpr uint64_t kBackBits = 0;
+  static constexpr int kParts = 4;           // a parse unit = one frame header byte
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
+  __device__ static __forceinline__ void frame(uint32_t h, uint32_t& L, uint32_t& bw) {
+    L = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
+    bw = ((h >> 2) & 31u) + 1u;
+  }
   __device__ static WAgg agg(const WCtx& c) {
-    uint32_t q = 0, d = 0;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t h = (c.w >> (8 * i)) & 0xFFu;
-      uint32_t L = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
-      uint32_t bw = ((h >> 2) & 31u) + 1u;
-      q += L;
-      d += 32u * ((L * bw + 31u) / 32u);
-    }
-    return WAgg{q, d, 0u};
+    uint32_t L, bw;
+    frame((c.w >> (8 * c.part)) & 0xFFu, L, bw);
+    return WAgg{L, 32u * ((L * bw + 31u) / 32u), 0u};
   }
   __device__ static bool suspect(const WCtx& c) {  // length code 3 or bit 7
     return ((c.w & (c.w >> 1) & 0x01010101u) | (c.w & 0x80808080u)) != 0;
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
-    uint32_t q = 0;
-    int32_t d = 0;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t h = (c.w >> (8 * i)) & 0xFFu;
-      Grp g = grp0();
-      g.q0 = q;
-      g.nq = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
-      g.bw = ((h >> 2) & 31u) + 1u;
-      g.step = g.bw;
-      g.d0 = d;
-      g.dlen = 32u * ((g.nq * g.bw + 31u) / 32u);
-      g.err = ((h & 3u) == 3u || (h & 0x80u)) ? GC_DEV_BAD_FRAME : 0u;
-      f(g);
-      q += g.nq;
-      d += (int32_t)g.dlen;
-    }
+    const uint32_t h = (c.w >> (8 * c.part)) & 0xFFu;
+    Grp g = grp0();
+    frame(h, g.nq, g.bw);
+    g.step = g.bw;
+    g.dlen = 32u * ((g.nq * g.bw + 31u) / 32u);
+    g.err = ((h & 3u) == 3u || (h & 0x80u)) ? GC_DEV_BAD_FRAME : 0u;
+    f(g);
   }
 };
 
@@ -382,7 +376,8 @@ struct CodecAFOR {
 template <int F>
 struct CodecPFD {
   static constexpr bool kExc = true;
-  static constexpr int kParts = 1;
+  static constexpr uint64_t kBackBits = 0;
+  static constexpr int kParts = F / 8;        // a parse unit = 8 quads of one frame
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
@@ -399,16 +394,19 @@ struct CodecPFD {
     if (cnt > 4 * q || (cnt > 0 && wc == 0)) g.err |= GC_DEV_BAD_EXCEPTION;
     g.bw = (b >= 1 && b <= 32) ? b : 32u;
     g.step = g.bw;
-    g.nq = F;
-    g.dlen = 32u * ((q * g.bw + 31u) / 32u);
+    g.fq = q;
+    g.dlen = 32u * ((q * g.bw + 31u) / 32u);   // the frame's data: fresh vectors
     g.wb = wc == 1 ? 1u : (wc == 2 ? 2u : (wc == 3 ? 4u : 0u));
     g.cnt = g.err ? 0u : cnt;
     g.elen = cnt * (kPosBytes + g.wb);
   }
+  // part p covers frame quads [8p, 8p+8): 8*b data lane-bits each, the frame's padding to
+  // whole vectors and all its exception bytes charged to the last / first part
   __device__ static WAgg agg(const WCtx& c) {
     Grp g = grp0();
     decode_hdr(c, g);
-    return WAgg{(uint32_t)F, g.dlen, g.elen};
+    const uint32_t d = c.part + 1 < (uint32_t)kParts ? 8u * g.bw : g.dlen - 8u * g.bw * (kParts - 1);
+    return WAgg{8u, d, c.part == 0 ? g.elen : 0u};
   }
   __device__ static bool suspect(const WCtx& c) {
     Grp g = grp0();
@@ -419,6 +417,14 @@ struct CodecPFD {
   __device__ static void walk(const WCtx& c, F2&& f) {
     Grp g = grp0();
     decode_hdr(c, g);
+    const uint32_t elen = g.elen;
+    g.t0 = 8u * c.part;
+    g.nq = 8u;
+    // data this part really needs (the bounds check), and the frame's exception area
+    // relative to the part's exception prefix (parts after the first follow it)
+    g.dlen = g.fq > g.t0 ? min(8u, g.fq - g.t0) * g.bw : 0u;
+    g.elen = c.part == 0 ? elen : 0u;
+    g.e0 = c.part == 0 ? 0u : 0u - elen;
     f(g);
   }
 };

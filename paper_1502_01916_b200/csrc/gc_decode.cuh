@@ -1,568 +1,485 @@
-// gc_decode.cuh -- k_decode (subsystems (b)-(d)); included inside namespace gcd by
-// gc_kernels.cu.
+// gc_decode.cuh -- k_decode (subsystems (b)-(d)); included inside
+// namespace gcd by gc_kernels.cu.
 //
-// Persistent warps.  A warp repeatedly claims an output warp-tile t (atomic counter, so
-// tiles start in order and the decoupled look-back always makes progress) and decodes the
-// quadruples containing the output positions [t*kT, (t+1)*kT) with warp-shuffle scans
-// only: no block barriers.  In-tile arithmetic is 32-bit and relative to the tile's staged
-// bases; the tile's lists live in a per-warp shared-memory table.
+// Output-space tiles: tile t owns the output ints [t*kT, (t+1)*kT) exactly and decodes
+// every quadruple holding one of them (a quad straddling a tile edge is decoded by both
+// tiles; each keeps its own ints).  One CTA of kThreads threads decodes one tile at a
+// time.  Tiles are assigned round-robin (tile = blockIdx.x + i*gridDim.x) to a
+// cooperative (co-resident) grid, so the next tile's entries and copies are known early
+// and the decoupled look-back always makes progress.  Per tile:
+//   1. Entry[t], Entry[t+1] (index kernel) give the tile's control words, data vectors and
+//      exception bytes, staged into shared memory by 1-D bulk async copies (TMA engine)
+//      issued while the previous tile was being stored.
+//   2. List table: the lists the tile touches (rounds of kLC) with their kept quads; the
+//      list starts inside the tile go to a reset bitmap.
+//   3. Parse + unpack: thread-blocked parse units (a control word or a fixed part of one).
+//      A block scan segmented at list starts gives each unit its quad / data / exception
+//      prefix; the unit's thread then unpacks its kept quads straight into the staging
+//      window: per lane the paper's high-first split is shl/shr/select;
+//      Group-PFD exceptions of the unit overwrite their slots.
+//   4. d-gap scan: 32 consecutive staged ints per thread, serial, then across the
+//      block (segmented by the reset bitmap), then across tiles (decoupled look-back).
+//   5. Stores: 128-bit streaming stores, carry-free chunks first, the chunks before the
+//      tile's first list start after the look-back.
 
-struct WarpSmem {  // per-warp shared memory, byte offsets
-  static constexpr uint32_t kOut = 0;                            // swizzled staging window
-  static constexpr uint32_t kDesc = kOut + kOutChunks * 16;      // uint2 per quad of a window
-  static constexpr uint32_t kData = kDesc + kRQ * 8;             // data vectors (+1 slack)
-  static constexpr uint32_t kCtrl = kData + (kDCap + 1) * 16;    // control words
-  static constexpr uint32_t kLt = kCtrl + kCCap * 4;             // list table (SoA)
-  static constexpr uint32_t kLtFields = 9;
-  static constexpr uint32_t kEnt = (kLt + kLtFields * (kLT + 1) * 4 + 15) & ~15u;  // 2 Entries
-  static constexpr uint32_t kXinfo = kEnt + 2 * sizeof(Entry);   // PFD per-quad info
-  __host__ __device__ static constexpr uint32_t exc_off() { return (kXinfo + kRQ * 4 + 15) & ~15u; }
+__host__ __device__ constexpr uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
+constexpr uint32_t kHalo = 32;                     // staging index = tile position + kHalo
+constexpr uint32_t kStW = kHalo + kT + 8;          // staging ints
+struct DS {  // dynamic shared memory layout (byte offsets)
+  static constexpr uint32_t kOut = 0;                                 // kStW u32, swizzled
+  static constexpr uint32_t kData = al128(kOut + kStW * 4);           // (kDCap + 1) uint4
+  static constexpr uint32_t kCtrl = al128(kData + (kDCap + 1) * 16);  // kCCap u32
+  static constexpr uint32_t kLtF = 8;                                 // list table fields
+  static constexpr uint32_t kLt = al128(kCtrl + kCCap * 4);           // kLtF x (kLC + 1) u32
+  static constexpr uint32_t kRst = al128(kLt + kLtF * (kLC + 1) * 4);  // kT/32 u32 bitmap
+  static constexpr uint32_t kExcB = al128(kRst + kT / 8);             // kECap bytes (PFD)
   __host__ __device__ static constexpr uint32_t bytes(bool exc) {
-    return exc ? ((exc_off() + kECap + 127) & ~127u) : ((kXinfo + 127) & ~127u);
+    return exc ? al128(kExcB + kECap) : kExcB;
   }
 };
 
-// In-tile scan state: f = a list starts in the range, q = raw quads of the list, d = data
-// lane-bits and e = exception bytes, both relative to the tile's staged bases.
-struct St {
-  uint32_t f, q, d, e;
-};
-__device__ __forceinline__ St st_op(const St& a, const St& b) {
-  return b.f ? b : St{a.f, a.q + b.q, a.d + b.d, a.e + b.e};
-}
-// Warp-wide exclusive segmented scan; *total = the warp aggregate.
-template <bool kExc>
-__device__ __forceinline__ St warp_excl_st(St v, St* total) {
-  const int lane = threadIdx.x & 31;
-  St inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    St n;
-    n.f = __shfl_up_sync(0xffffffffu, inc.f, o);
-    n.q = __shfl_up_sync(0xffffffffu, inc.q, o);
-    n.d = __shfl_up_sync(0xffffffffu, inc.d, o);
-    n.e = kExc ? __shfl_up_sync(0xffffffffu, inc.e, o) : 0u;
-    if (lane >= o) inc = st_op(n, inc);
-  }
-  total->f = __shfl_sync(0xffffffffu, inc.f, 31);
-  total->q = __shfl_sync(0xffffffffu, inc.q, 31);
-  total->d = __shfl_sync(0xffffffffu, inc.d, 31);
-  total->e = kExc ? __shfl_sync(0xffffffffu, inc.e, 31) : 0u;
-  St ex;
-  ex.f = __shfl_up_sync(0xffffffffu, inc.f, 1);
-  ex.q = __shfl_up_sync(0xffffffffu, inc.q, 1);
-  ex.d = __shfl_up_sync(0xffffffffu, inc.d, 1);
-  ex.e = kExc ? __shfl_up_sync(0xffffffffu, inc.e, 1) : 0u;
-  if (lane == 0) ex = St{0, 0, 0, 0};
-  return ex;
-}
-__device__ __forceinline__ uint32_t warp_excl_sum(uint32_t v, uint32_t* total) {
-  const int lane = threadIdx.x & 31;
-  uint32_t inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t n = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += n;
-  }
-  *total = __shfl_sync(0xffffffffu, inc, 31);
-  return inc - v;
-}
-__device__ __forceinline__ Seg1 warp_excl_seg1(Seg1 x, Seg1* total) {
-  const int lane = threadIdx.x & 31;
-  Seg1 inc = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    Seg1 n;
-    n.f = __shfl_up_sync(0xffffffffu, inc.f, o);
-    n.v = __shfl_up_sync(0xffffffffu, inc.v, o);
-    if (lane >= o) inc = seg1_op(n, inc);
-  }
-  total->f = __shfl_sync(0xffffffffu, inc.f, 31);
-  total->v = __shfl_sync(0xffffffffu, inc.v, 31);
-  Seg1 ex;
-  ex.f = __shfl_up_sync(0xffffffffu, inc.f, 1);
-  ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
-  if (lane == 0) ex = Seg1{0, 0};
-  return ex;
+// Staging swizzle: 16-B chunk c lives at chunk c ^ ((c >> 3) & 7), which keeps the blocked
+// (8 chunks per thread) and striped (one chunk per thread) 128-bit accesses conflict-free
+// and spreads the scalar writes of thread-serial runs.
+__device__ __forceinline__ uint32_t sw_chunk(uint32_t c) { return c ^ ((c >> 3) & 7u); }
+__device__ __forceinline__ uint32_t sw_word(uint32_t x) {
+  return (sw_chunk(x >> 2) << 2) | (x & 3u);
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Stream ranges of one tile (set up by one thread from the tile's two entries).
+struct Geo {
+  uint32_t ok, k0, k1, ctrl_st;
+  uint32_t data_st, exc_st, pad0, pad1;
+  uint64_t wa, wb, cbase, cstop, va, vb, ea, eb, la, lb;
+  Seg4 seed;  // (list start flag, raw quads, data lane-bits, exception bytes) at word wa
+};
+
 #ifndef GC_DECODE_MINB
-#define GC_DECODE_MINB 2
+#define GC_DECODE_MINB 3
 #endif
-template <class C, bool DGAPS, int kWPC>
-__global__ void __launch_bounds__(32 * kWPC, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t smem_all[];
-  __shared__ __align__(8) uint64_t s_bar[kWPC];
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint8_t* smem = smem_all + wid * WarpSmem::bytes(C::kExc);
-  uint4* s_out4 = reinterpret_cast<uint4*>(smem + WarpSmem::kOut);
-  uint32_t* s_out = reinterpret_cast<uint32_t*>(smem + WarpSmem::kOut);
-  uint2* s_desc = reinterpret_cast<uint2*>(smem + WarpSmem::kDesc);
-  uint4* s_data = reinterpret_cast<uint4*>(smem + WarpSmem::kData);
-  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(smem + WarpSmem::kCtrl);
-  uint32_t* s_lt = reinterpret_cast<uint32_t*>(smem + WarpSmem::kLt);
-  uint32_t* lt_cw = s_lt + 0 * (kLT + 1);     // first control word (relative to cbase)
-  uint32_t* lt_q = s_lt + 1 * (kLT + 1);      // quads
-  uint32_t* lt_n = s_lt + 2 * (kLT + 1);      // ints
-  uint32_t* lt_klo = s_lt + 3 * (kLT + 1);    // first quad owned by the tile
-  uint32_t* lt_kend = s_lt + 4 * (kLT + 1);   // one past the last
-  uint32_t* lt_oref = s_lt + 5 * (kLT + 1);   // staging index of quad j = oref + 4j
-  uint32_t* lt_db = s_lt + 6 * (kLT + 1);     // staged data lane-bit of the list start
-  uint32_t* lt_eb = s_lt + 7 * (kLT + 1);     // staged exception byte of the list start
-  uint32_t* lt_lb = s_lt + 8 * (kLT + 1);     // local index of quad klo within the round
-  uint32_t* s_ent = reinterpret_cast<uint32_t*>(smem + WarpSmem::kEnt);
-  uint32_t* s_xinfo = reinterpret_cast<uint32_t*>(smem + WarpSmem::kXinfo);
-  uint8_t* s_exc = smem + WarpSmem::exc_off();
-  uint64_t* bar = &s_bar[wid];
-  if (lane == 0) mbar_init(bar, 1);
-  __syncwarp();
-  uint32_t phase = 0;
-  uint32_t err = 0;
+template <class C, bool DGAPS>
+__global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS::kOut);
+  uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS::kOut);
+  uint4* s_data = reinterpret_cast<uint4*>(sm + DS::kData);
+  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(sm + DS::kCtrl);
+  uint32_t* s_lt = reinterpret_cast<uint32_t*>(sm + DS::kLt);
+  uint32_t* s_rst = reinterpret_cast<uint32_t*>(sm + DS::kRst);
+  uint8_t* s_exc = sm + DS::kExcB;
+  uint32_t* lt_cw = s_lt + 0 * (kLC + 1);    // first control word, relative to cbase (wraps)
+  uint32_t* lt_q = s_lt + 1 * (kLC + 1);     // quads
+  uint32_t* lt_n = s_lt + 2 * (kLC + 1);     // ints
+  uint32_t* lt_klo = s_lt + 3 * (kLC + 1);   // first quad kept by the tile
+  uint32_t* lt_kend = s_lt + 4 * (kLC + 1);  // one past the last
+  uint32_t* lt_oref = s_lt + 5 * (kLC + 1);  // staging index of quad j = oref + 4j (wraps)
+  uint32_t* lt_db = s_lt + 6 * (kLC + 1);    // data lane-bit of the list start, rel. to va*32
+  uint32_t* lt_eb = s_lt + 7 * (kLC + 1);    // exception byte of the list start, rel. to ea
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(16) Entry s_e[2];   // entries of the next tile
+  __shared__ Geo s_g[2];                   // geometry of the current / next tile
+  __shared__ Seg4 s_scr4[kWarps];
+  __shared__ Seg1 s_scr1[kWarps];
+  __shared__ uint32_t s_reset0[2], s_cin;
 
-  // 128-bit store of staging chunk c (the 16-B output block 4c..4c+3 clipped to [lo, hi));
-  // ints before staging index r0 get the look-back carry cin
-  auto store_chunk = [&](int64_t c, int64_t cb, int64_t lo, int64_t hi, uint32_t cin, uint32_t r0) {
-    const uint32_t lc = (uint32_t)(c - cb);
-    uint4 v = s_out4[sw_chunk(lc)];
-    if (cin) {
-      const uint32_t p = 4 * lc;
-      if (p < r0) v.x += cin;
-      if (p + 1 < r0) v.y += cin;
-      if (p + 2 < r0) v.z += cin;
-      if (p + 3 < r0) v.w += cin;
-    }
-    const int64_t g = 4 * c;
-    if (g >= lo && g + 4 <= hi) {
-      __stcs(reinterpret_cast<uint4*>(out + g), v);
-    } else {
-      const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
-      for (int k = 0; k < 4; k++)
-        if (g + k >= lo && g + k < hi) out[g + k] = a4[k];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
+  const uint64_t dend = D.data_off[D.n_lists];
+  const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
+  uint32_t phase = 0, err = 0;
+
+  // Entries of `tile` -> s_e (one warp)
+  auto load_entries = [&](uint32_t tile) {
+    if (tile < D.n_tiles_b) {
+      if (lane < 16) {
+        reinterpret_cast<uint32_t*>(s_e)[lane] =
+            reinterpret_cast<const uint32_t*>(D.entries + tile)[lane];
+      } else if (tile + 1 < D.n_tiles_b) {
+        reinterpret_cast<uint32_t*>(s_e)[lane] =
+            reinterpret_cast<const uint32_t*>(D.entries + tile + 1)[lane - 16];
+      }
     }
   };
-  // A tile whose first list segment needs the carry of earlier tiles is finished only after
-  // this warp has claimed and set up its next tile, so the look-back wait overlaps that
-  // tile's bulk copies (its staging window is not touched before then).
-  bool pd_on = false;
-  uint32_t pd_tile = 0, pd_reset0 = 0, pd_f = 0, pd_v = 0;
-  int64_t pd_lo = 0, pd_hi = 0, pd_clo = 0, pd_cmid = 0, pd_cb = 0;
-  auto finish_pending = [&]() {
-    if (!pd_on) return;
-    const uint32_t cin = lookback_u32(D.tiles_b, pd_tile);
-    if (lane == 0 && !pd_f)
-      st_relaxed_u64(D.tiles_b + pd_tile, ((uint64_t)kFlagIncl << 32) | (cin + pd_v));
-    for (int64_t c = pd_clo + lane; c < pd_cmid; c += 32) store_chunk(c, pd_cb, pd_lo, pd_hi, cin, pd_reset0);
-    pd_on = false;
-    __syncwarp();
+  // One thread: the tile's stream ranges from s_e -> s_g[buf], and the bulk async copies
+  // of its control / exception bytes (barrier 0) and data (barrier 1).  A tile past the
+  // end or with bad entries arms both barriers with 0 bytes.
+  auto setup = [&](uint32_t tile, uint32_t buf) {
+    Geo& g = s_g[buf];
+    const Entry& E0 = s_e[0];
+    const Entry& E1 = s_e[1];
+    const bool last = tile + 1 == D.n_tiles_b;
+    g.ok = 0;
+    uint32_t cbytes = 0, xbytes = 0, dbytes = 0;
+    if (tile < D.n_tiles_b) {
+      const uint64_t wa = E0.w, wb = last ? cend - 1 : E1.w;
+      g.ok = (E0.valid && (last || E1.valid) && wb >= wa && wb < D.n_ctrl_words &&
+              E0.l < D.n_lists && (last || (E1.l >= E0.l && E1.l < D.n_lists))) ? 1u : 0u;
+      if (!g.ok) atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
+    }
+    if (g.ok) {
+      const uint64_t wa = E0.w, wb = last ? cend - 1 : E1.w;
+      g.wa = wa;
+      g.wb = wb;
+      g.cbase = (wa ? wa - 1 : 0) & ~3ull;
+      g.cstop = mn64((wb + 4) & ~3ull, D.n_ctrl_words);
+      g.ctrl_st = g.cstop - g.cbase <= kCCap;
+      // a group may start before its word's data prefix (complete unary: up to CG*32 lane
+      // bits, the code's start in the previous word)
+      g.va = (E0.wd - mn64(E0.wd, C::kBackBits)) >> 5;
+      g.vb = mx64(g.va, mn64(last ? dend : (E1.wd_end + 31) >> 5, D.data_vectors));
+      g.data_st = g.vb - g.va <= kDCap;
+      g.ea = g.eb = 0;
+      g.exc_st = 0;
+      if (C::kExc) {
+        g.ea = E0.we & ~15ull;
+        g.eb = mx64(g.ea, mn64(((last ? eend : E1.we_end) + 15) & ~15ull, D.exc_bytes));
+        g.exc_st = g.eb - g.ea <= kECap;
+      }
+      g.la = E0.l;
+      g.lb = last ? D.n_lists - 1 : E1.l;
+      g.k0 = E0.k;
+      g.k1 = last ? 0x7FFFFFFFu : E1.k;  // (the last tile keeps every quad of its last list)
+      g.seed = Seg4{1u, E0.wq, (uint32_t)(E0.wd - g.va * 32ull), (uint32_t)(E0.we - g.ea)};
+      cbytes = g.ctrl_st ? (uint32_t)(g.cstop - g.cbase) * 4 : 0u;
+      xbytes = g.exc_st ? (uint32_t)(g.eb - g.ea) : 0u;
+      dbytes = g.data_st ? (uint32_t)(g.vb - g.va) * 16 : 0u;
+    }
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar[0], cbytes + xbytes);
+    if (cbytes) bulk_g2s(s_ctrl, D.ctrl_words + g.cbase, cbytes, &s_bar[0]);
+    if (xbytes) bulk_g2s(s_exc, D.exc + g.ea, xbytes, &s_bar[0]);
+    mbar_expect_tx(&s_bar[1], dbytes);
+    if (dbytes) bulk_g2s(s_data, D.data + g.va, dbytes, &s_bar[1]);
   };
 
-  while (true) {
-    // ---------------------------------------------------------------- claim a tile
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&D.hdr->counter_b, 1u);
-    tile = __shfl_sync(0xffffffffu, tile, 0);
-    if (tile >= D.n_tiles_b) {
-      finish_pending();
-      break;
-    }
-    // the two boundary Entries (80 B each) -> shared, 20 lanes x 2 words
-    {
-      const uint32_t* e0p = reinterpret_cast<const uint32_t*>(D.entries + tile);
-      if (lane < 20) {
-        s_ent[lane] = e0p[lane];
-        if (tile + 1 < D.n_tiles_b) s_ent[20 + lane] = e0p[20 + lane];
-      }
-      __syncwarp();
-    }
-    const Entry& E0 = *reinterpret_cast<const Entry*>(s_ent);
-    Entry E1;
-    if (tile + 1 < D.n_tiles_b) {
-      E1 = *reinterpret_cast<const Entry*>(s_ent + 20);
-    } else {
-      E1.l = (uint32_t)D.n_lists;
-      E1.j = 0;
-      E1.valid = 1;
-      E1.cend = D.ctrl_off[D.n_lists] >> 2;
-      E1.dend = D.data_off[D.n_lists] * 32ull;
-      E1.eend = D.exc_off ? D.exc_off[D.n_lists] : 0ull;
-    }
-    const int64_t base_int = (int64_t)tile * kT - 4;  // global int at staging index 0
-    if (!(E0.valid && E1.valid && E1.cend > E0.gword && E0.l < D.n_lists)) {
-      if (lane == 0) {
-        atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
-        if (DGAPS) st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
-      }
-      __syncwarp();
-      continue;
-    }
-    // ---------------------------------------------------------------- stream ranges
-    const uint64_t wa = E0.gword, wb = E1.cend;
-    const uint64_t cbase = (wa ? wa - 1 : 0) & ~3ull;
-    const uint64_t cstop = mn64((wb + 3) & ~3ull, D.n_ctrl_words);
-    const bool ctrl_staged = cstop - cbase <= kCCap;
-    const uint64_t va = E0.dbeg >> 5;
-    const uint64_t vb = mx64(va, mn64((E1.dend + 31) >> 5, D.data_vectors));
-    const bool data_staged = vb - va <= kDCap;
-    uint64_t ea = 0, eb = 0;
-    bool exc_staged = false;
-    if (C::kExc) {
-      ea = E0.ebeg & ~15ull;
-      eb = mx64(ea, mn64((E1.eend + 15) & ~15ull, D.exc_bytes));
-      exc_staged = eb - ea <= kECap;
-    }
-    if (lane == 0) {
-      uint32_t bytes = 0;
-      if (ctrl_staged && cstop > cbase) bytes += (uint32_t)(cstop - cbase) * 4;
-      if (data_staged && vb > va) bytes += (uint32_t)(vb - va) * 16;
-      if (C::kExc && exc_staged && eb > ea) bytes += (uint32_t)(eb - ea);
-      fence_proxy_async_smem();
-      mbar_expect_tx(bar, bytes);
-      if (ctrl_staged && cstop > cbase)
-        bulk_g2s(s_ctrl, D.ctrl_words + cbase, (uint32_t)(cstop - cbase) * 4, bar);
-      if (data_staged && vb > va) bulk_g2s(s_data, D.data + va, (uint32_t)(vb - va) * 16, bar);
-      if (C::kExc && exc_staged && eb > ea) bulk_g2s(s_exc, D.exc + ea, (uint32_t)(eb - ea), bar);
-    }
-    finish_pending();  // the previous tile's look-back, now that this tile's copies are in flight
-    const uint32_t ncw = (uint32_t)(cstop - cbase);
-    const uint32_t* cwp = ctrl_staged ? s_ctrl : D.ctrl_words + cbase;  // word w at cwp[w-cbase]
-    const uint4* dptr = data_staged ? s_data : D.data + va;
-    const uint8_t* eptr = exc_staged ? s_exc : D.exc + ea;
-    const uint32_t dlim = (uint32_t)mn64(vb - va, 0x7FFFFFFFull);
-    const uint32_t elim = (uint32_t)mn64(eb - ea, 0x7FFFFFFFull);
+  // prologue: the first tile's entries and copies
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+  }
+  if (warp == 0) load_entries(blockIdx.x);
+  if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kThreads words
+  if (tid == 0) s_reset0[0] = kT;
+  __syncthreads();
+  if (tid == 0) setup(blockIdx.x, 0);
+  __syncthreads();
 
-    // ---------------------------------------------------------------- output window
-    int64_t out_lo = (int64_t)(D.out_off[E0.l] + 4ull * E0.j);
-    int64_t out_hi = E1.l < D.n_lists ? (int64_t)(D.out_off[E1.l] + 4ull * E1.j) : (int64_t)D.total_out;
-    {
-      const int64_t clo = smax64(base_int, 0);
-      const int64_t chi = smin64(base_int + kOutWords, (int64_t)D.total_out);
-      if (out_lo < clo || out_hi > chi || out_hi < out_lo) {
-        err |= GC_DEV_TRUNCATED;
-        out_lo = smax64(out_lo, clo);
-        out_hi = smax64(out_lo, smin64(out_hi, chi));
-      }
+  uint32_t buf = 0;
+  for (uint32_t tile = blockIdx.x; tile < D.n_tiles_b; tile += gridDim.x, buf ^= 1u) {
+    // warp 1 prefetches the next tile's entries (read after this tile's unpack)
+    if (warp == 1) load_entries(tile + gridDim.x);
+    if (tid == 0) s_reset0[buf ^ 1u] = kT;  // the next tile's
+    const Geo& G = s_g[buf];
+    const bool ok = G.ok;
+    const bool last = tile + 1 == D.n_tiles_b;
+    const uint64_t tT = (uint64_t)tile * kT;
+    uint64_t cbase = 0, va = 0, ea = 0, la = 0, nl = 0;
+    uint32_t ncw = 0, dlim = 1, elim = 0, E0k = 0, E1k = 0, rwa = 0, rwb = 0;
+    bool data_st = false;
+    const uint32_t* cwp = D.ctrl_words;
+    const uint8_t* eptr = D.exc;
+    Seg4 seed{0u, 0u, 0u, 0u};
+    if (ok) {
+      cbase = G.cbase;
+      va = G.va;
+      ea = G.ea;
+      la = G.la;
+      nl = G.lb - G.la + 1;
+      ncw = (uint32_t)(G.cstop - cbase);
+      dlim = (uint32_t)mn64(mx64(G.vb - va, 1), 0x7FFFFFFFull);
+      elim = (uint32_t)mn64(G.eb - ea, 0x7FFFFFFFull);
+      data_st = G.data_st;
+      cwp = G.ctrl_st ? s_ctrl : D.ctrl_words + cbase;  // word w at cwp[w - cbase]
+      eptr = G.exc_st ? s_exc : D.exc + ea;
+      E0k = G.k0;
+      E1k = G.k1;
+      seed = G.seed;
+      rwa = (uint32_t)(G.wa - cbase);
+      rwb = (uint32_t)(G.wb + 1 - cbase);
     }
-    const uint32_t lo_loc = (uint32_t)(out_lo - base_int), hi_loc = (uint32_t)(out_hi - base_int);
-    const uint64_t lf = E0.l, ll = E1.l;
-    const uint32_t j0 = E0.j, j1 = E1.j;
-    const uint64_t lend = j1 > 0 && ll < D.n_lists ? ll + 1 : ll;
-    const uint32_t nlists = (uint32_t)(lend - lf);
-    const St carry0{1u, E0.wq, (uint32_t)(E0.wd - va * 32ull), (uint32_t)(E0.we - ea)};
-    __syncwarp();  // everyone has read s_ent
+    const uint64_t lb = la + nl - 1;
+    bool w0done = false, w1done = false;
 
-    Seg1 rcarry{0u, 0u};  // d-gap running state across windows
-    uint32_t reset0 = hi_loc;  // staging index of the tile's first list start
-    bool waited = false;
+    // one quad: 4 values of BW bits at data lane-bit pos; their ints go to staging
+    // indices idx .. idx + min(4, rem) - 1
+    auto unpack_quad = [&](uint32_t pos, uint32_t bw, uint32_t idx, uint32_t rem, auto staged) {
+      constexpr bool kStaged = decltype(staged)::value;
+      const uint32_t m = min(pos >> 5, dlim - 1u), off = pos & 31u;
+      uint4 v0, v1;
+      if constexpr (kStaged) {
+        v0 = s_data[m];
+        v1 = s_data[m + 1];  // slack vector past the staged range
+      } else {
+        v0 = __ldg(D.data + va + m);
+        v1 = __ldg(D.data + va + min(m + 1, dlim - 1u));
+      }
+      // the value's high part is the top of the current component, its low part the
+      // bottom of the next vector's component
+      const bool strad = off + bw > 32u;
+      const uint32_t shl = strad ? 0u : 32u - off - bw, shr = 32u - bw;
+      const uint32_t ml = strad ? (1u << (off + bw - 32u)) - 1u : 0u;
+      const uint32_t x0 = (((v0.x << shl) >> shr) & ~ml) | (v1.x & ml);
+      const uint32_t x1 = (((v0.y << shl) >> shr) & ~ml) | (v1.y & ml);
+      const uint32_t x2 = (((v0.z << shl) >> shr) & ~ml) | (v1.z & ml);
+      const uint32_t x3 = (((v0.w << shl) >> shr) & ~ml) | (v1.w & ml);
+      idx = min(idx, kStW - 4u);
+      if (rem >= 4u && (idx & 3u) == 0) {
+        s_out4[sw_chunk(idx >> 2)] = make_uint4(x0, x1, x2, x3);
+      } else {
+        s_out[sw_word(idx)] = x0;
+        if (rem > 1u) s_out[sw_word(idx + 1)] = x1;
+        if (rem > 2u) s_out[sw_word(idx + 2)] = x2;
+        if (rem > 3u) s_out[sw_word(idx + 3)] = x3;
+      }
+    };
 
-    for (uint32_t lr = 0; lr < nlists; lr += kLT) {
+    for (uint64_t lr = 0; lr < nl; lr += kLC) {
       // ---------------------------------------------------------------- list table
-      const uint32_t cnt = min(kLT, nlists - lr);
-      uint32_t kept = 0;
-      {
-        const uint64_t l = lf + lr + lane;
-        if (lane <= cnt) lt_cw[lane] = (uint32_t)((D.ctrl_off[mn64(l, D.n_lists)] >> 2) - cbase);
-        if (lane == 0 && cnt == 32) lt_cw[32] = (uint32_t)((D.ctrl_off[mn64(l + 32, D.n_lists)] >> 2) - cbase);
-        if (lane < cnt) {
-          const uint32_t n = D.list_n[l];
-          const uint32_t Q = (n + 3) >> 2;
-          const uint32_t klo = l == lf ? j0 : 0u;
-          const uint32_t kend = l == ll ? min(Q, j1) : Q;
-          lt_q[lane] = Q;
-          lt_n[lane] = n;
-          lt_klo[lane] = klo;
-          lt_kend[lane] = kend;
-          lt_oref[lane] = l == lf ? lo_loc - 4u * j0 : (uint32_t)((int64_t)D.out_off[l] - base_int);
-          lt_db[lane] = (uint32_t)(D.data_off[l] * 32ull - va * 32ull);
-          lt_eb[lane] = C::kExc ? (uint32_t)(D.exc_off[l] - ea) : 0u;
-          kept = kend > klo ? kend - klo : 0u;
+      const uint32_t cnt = (uint32_t)mn64(kLC, nl - lr);
+      if (lr) __syncthreads();  // the previous list round is done with the table
+      if (tid < cnt) {
+        const uint64_t l = la + lr + tid;
+        const uint32_t n = D.list_n[l];
+        const uint32_t Q = (n + 3) >> 2;
+        const uint32_t klo = l == la ? E0k : 0u;
+        const uint32_t kend = l == lb ? min(Q, E1k + 1) : Q;
+        const uint32_t oref = (uint32_t)(D.out_off[l] - tT + kHalo);
+        lt_cw[tid] = (uint32_t)((D.ctrl_off[l] >> 2) - cbase);
+        lt_q[tid] = Q;
+        lt_n[tid] = n;
+        lt_klo[tid] = klo;
+        lt_kend[tid] = kend;
+        lt_oref[tid] = oref;
+        lt_db[tid] = (uint32_t)(D.data_off[l] * 32ull - va * 32ull);
+        lt_eb[tid] = C::kExc ? (uint32_t)(D.exc_off[l] - ea) : 0u;
+        // a list that starts inside the tile resets the d-gap scan
+        if (DGAPS && n > 0 && klo == 0 && oref >= kHalo && oref < kHalo + kT) {
+          atomicOr(&s_rst[(oref - kHalo) >> 5], 1u << ((oref - kHalo) & 31u));
+          atomicMin(&s_reset0[buf], oref - kHalo);
         }
       }
-      uint32_t K;
-      const uint32_t lbk = warp_excl_sum(kept, &K);
-      if (lane < cnt) lt_lb[lane] = lbk;
-      if (!waited) {
-        mbar_wait(bar, phase);
-        waited = true;
+      if (tid == 0) lt_cw[cnt] = lr + cnt < nl ? (uint32_t)((D.ctrl_off[la + lr + cnt] >> 2) - cbase) : rwb;
+      if (!w0done) {
+        mbar_wait(&s_bar[0], phase);
+        w0done = true;
       }
-      __syncwarp();
+      __syncthreads();
+      const uint32_t rw0 = lr == 0 ? rwa : lt_cw[0];
+      const uint32_t rw1 = lt_cw[cnt];
 
-      const uint64_t rw0 = lr == 0 ? wa : cbase + lt_cw[0];
-      const uint64_t rw1 = mn64(wb, cbase + lt_cw[cnt]);
-
-      for (uint32_t u = 0; u < K; u += kRQ) {
-        St carry = carry0;
-        // control units (a word, or a kParts-th of one) in rounds of 32 x kCBW
-        constexpr uint32_t P = C::kParts;
-        const uint64_t ru0 = rw0 * P, ru1 = rw1 * P;
-        for (uint64_t r0 = ru0; r0 < ru1; r0 += kRoundWords) {
-          const uint64_t my0 = r0 + (uint64_t)lane * kCBW;
-          const uint32_t myn = my0 < ru1 ? (uint32_t)mn64(kCBW, ru1 - my0) : 0u;
-          uint32_t li = 0;
-          if (myn) {  // the last table entry whose first word is <= my first word
-            const uint32_t key = (uint32_t)(my0 / P - cbase);
-            uint32_t a = 0, b = cnt;
-            while (b - a > 1) {
-              const uint32_t m = (a + b) >> 1;
-              if (lt_cw[m] <= key) a = m;
-              else b = m;
-            }
-            li = a;
+      // -------------------------------------------------------------- parse + unpack
+      constexpr uint32_t P = C::kParts;
+      const uint32_t ru0 = rw0 * P, ru1 = rw1 * P;
+      const uint32_t nu = ru1 > ru0 ? ru1 - ru0 : 0u;
+      const uint32_t ku = max(1u, min(kUPT, (nu + kThreads - 1) / kThreads));
+      Seg4 carry = lr == 0 ? seed : Seg4{0u, 0u, 0u, 0u};
+      for (uint32_t cb0 = ru0; cb0 < ru1; cb0 += kThreads * ku) {
+        const uint32_t my0 = cb0 + tid * ku;
+        const uint32_t myn = my0 < ru1 ? min(ku, ru1 - my0) : 0u;
+        uint32_t li = 0;
+        if (myn) {  // the last table entry whose first word is <= my first word
+          const uint32_t key = my0 / P;
+          uint32_t a = 0, b = cnt;
+          while (b - a > 1) {
+            const uint32_t m = (a + b) >> 1;
+            if (lt_cw[m] <= key) a = m;
+            else b = m;
           }
-          uint32_t wv[kCBW], pv[kCBW], wl[kCBW];
-          St agg{0, 0, 0, 0};
+          li = a;
+        }
+        uint32_t wv[kUPT], pv[kUPT], wl[kUPT];
+        WAgg wg[kUPT];
+        Seg4 agg{0u, 0u, 0u, 0u};
 #pragma unroll
-          for (uint32_t k = 0; k < kCBW; k++) {
-            const uint64_t un = my0 + k;
-            const uint64_t w = un / P;
-            const uint32_t part = (uint32_t)(un % P);
-            const uint32_t wr = (uint32_t)(w - cbase);
-            wv[k] = pv[k] = wl[k] = 0;
-            if (k < myn) {
-              while (li + 1 < cnt && lt_cw[li + 1] <= wr) li++;
-              wl[k] = li;
-              wv[k] = wr < ncw ? cwp[wr] : 0u;
-              pv[k] = (C::kNeedsPrev && wr >= 1 && wr - 1 < ncw) ? cwp[wr - 1] : 0u;
-              const uint32_t widx = wr - lt_cw[li];
-              const WCtx c{wv[k], pv[k], widx, lt_q[li], part};
-              const WAgg a = C::agg(c);
-              agg = (widx == 0 && part == 0 && w != wa)
-                        ? St{1u, a.q, lt_db[li] + a.d, lt_eb[li] + a.e}
-                        : St{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
-            }
+        for (uint32_t k = 0; k < kUPT; k++) {
+          wv[k] = pv[k] = 0u;
+          wl[k] = li;
+          wg[k] = WAgg{0u, 0u, 0u};
+          if (k < myn) {
+            const uint32_t un = my0 + k, w = un / P, part = un % P;
+            while (li + 1 < cnt && lt_cw[li + 1] <= w) li++;
+            wl[k] = li;
+            wv[k] = w < ncw ? cwp[w] : 0u;
+            pv[k] = (C::kNeedsPrev && w >= 1 && w - 1 < ncw) ? cwp[w - 1] : 0u;
+            const uint32_t widx = w - lt_cw[li];
+            const WAgg a = C::agg(WCtx{wv[k], pv[k], widx, lt_q[li], part});
+            wg[k] = a;
+            agg = (widx == 0 && part == 0) ? Seg4{1u, a.q, lt_db[li] + a.d, lt_eb[li] + a.e}
+                                           : Seg4{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
           }
-          St rtot;
-          St S = st_op(carry, warp_excl_st<C::kExc>(agg, &rtot));
-          carry = st_op(carry, rtot);
-
-          // per-quad descriptors (position, width, staging slot) of the window's quads
+        }
+        Seg4 tot;
+        Seg4 S = seg4_op(carry, block_excl_seg4<C::kExc>(agg, s_scr4, &tot));
+        carry = seg4_op(carry, tot);
+        if (!w1done) {
+          mbar_wait(&s_bar[1], phase);
+          w1done = true;
+        }
+        auto units = [&](auto staged) {
 #pragma unroll
-          for (uint32_t k = 0; k < kCBW; k++) {
+          for (uint32_t k = 0; k < kUPT; k++) {
             if (k >= myn) break;
-            const uint64_t un = my0 + k;
-            const uint64_t w = un / P;
-            const uint32_t part = (uint32_t)(un % P);
-            const uint32_t wr = (uint32_t)(w - cbase);
+            const uint32_t un = my0 + k, w = un / P, part = un % P;
             const uint32_t i = wl[k];
-            const uint32_t widx = wr - lt_cw[i];
-            const WCtx c{wv[k], pv[k], widx, lt_q[i], part};
-            if (widx == 0 && part == 0 && w != wa) S = St{1u, 0u, lt_db[i], lt_eb[i]};
-            const WAgg a = C::agg(c);
-            const uint32_t klo = lt_klo[i], kend = lt_kend[i];
-            const uint32_t qa = max(S.q, klo), qb = min(S.q + a.q, kend);
-            const uint32_t x0 = lt_lb[i] + (qa - klo);  // local index of quad qa
-            if (!(qb > qa && x0 < u + kRQ && x0 + (qb - qa) > u)) {
-            } else if constexpr (!C::kMultiQuad) {
-              // one quad per group: tight codec loop straight into the descriptors
-              const uint32_t ja = qa + (u > x0 ? u - x0 : 0u);
-              const uint32_t jb = min(qb, qa + (u + kRQ - x0));
+            const uint32_t widx = w - lt_cw[i];
+            if (widx == 0 && part == 0) S = Seg4{1u, 0u, lt_db[i], lt_eb[i]};
+            const WAgg a = wg[k];
+            const uint32_t qa = max(S.q, lt_klo[i]), qb = min(S.q + a.q, lt_kend[i]);
+            if (qb > qa) {
+              const WCtx c{wv[k], pv[k], widx, lt_q[i], part};
               const uint32_t n = lt_n[i], oref = lt_oref[i];
-              const uint32_t lbase = x0 - qa - u;  // descriptor slot of quad j = lbase + j
-              C::emit(c, S.q, S.d, ja, jb, [&](uint32_t j, uint32_t pos, uint32_t bw) {
-                const uint32_t op = oref + 4u * j;
-                const uint32_t cq = min(4u, n - 4u * j);
-                const uint32_t rst = j == 0 ? 1u : 0u;
-                s_desc[lbase + j] = make_uint2(pos, bw | (op << 6) | ((cq - 1) << 19) | (rst << 21));
-                if (DGAPS && rst) reset0 = min(reset0, op);
-              });
-            } else {
-              const St SW = S;
-              const uint32_t n = lt_n[i], oref = lt_oref[i], Qi = lt_q[i];
-              C::walk(c, [&](const Grp& g) {
-                const uint32_t gq = SW.q + g.q0;
-                const uint32_t ja = max(max(gq, qa), qa + (u > x0 ? u - x0 : 0u));
-                const uint32_t jb = min(min(gq + g.nq, qb), qa + (u + kRQ - x0));
-                if (ja >= jb) return;
-                const uint32_t gd = SW.d + (uint32_t)g.d0;
-                uint32_t ei = 0, erank = 0, pprev = 0;
-                const uint32_t qf = C::kExc ? min(g.nq, Qi - gq) : 0u;
-                for (uint32_t j = ja; j < jb; j++) {
-                  const uint32_t loc = x0 + (j - qa) - u;
-                  const uint32_t op = oref + 4u * j;
-                  const uint32_t cq = min(4u, n - 4u * j);
-                  const uint32_t rst = j == 0 ? 1u : 0u;
-                  if (op + cq > hi_loc || op < lo_loc) err |= GC_DEV_TRUNCATED;
-                  s_desc[loc] = make_uint2(gd + (j - gq) * g.step,
-                                           g.bw | (min(op, kOutWords - 4) << 6) |
-                                               ((cq - 1) << 19) | (rst << 21));
-                  if (DGAPS && rst) reset0 = min(reset0, op);
-                  if (C::kExc) {
-                    // exceptions of this quad: frame positions [4t, 4t+4)
-                    const uint32_t t4 = 4 * (j - gq);
-                    const uint32_t pb = 4 * g.nq <= 256 ? 1u : 2u;
+              if constexpr (!C::kMultiQuad) {
+                // one quad per group: the codec's tight loop straight into the unpack
+                C::emit(c, S.q, S.d, qa, qb, [&](uint32_t j, uint32_t pos, uint32_t bw) {
+                  unpack_quad(pos, bw, oref + 4u * j, n - 4u * j, staged);
+                });
+              } else {
+                const Seg4 SW = S;
+                C::walk(c, [&](const Grp& g) {
+                  const uint32_t gq = SW.q + g.q0;
+                  const uint32_t ja = max(gq, qa), jb = min(gq + g.nq, qb);
+                  if (ja >= jb) return;
+                  const uint32_t gd = SW.d + (uint32_t)g.d0;
+                  for (uint32_t j = ja; j < jb; j++)
+                    unpack_quad(gd + (j - gq) * g.step, g.bw, oref + 4u * j, n - 4u * j, staged);
+                  if constexpr (C::kExc) {
+                    // Group-PFD: the frame's exceptions in this unit's quads overwrite their
+                    // slots; positions are frame-relative ints, values follow them
+                    const uint32_t pb = C::kPosBytes;
                     const uint32_t e0 = SW.e + g.e0;
-                    uint32_t mask = 0;
-                    while (ei < g.cnt) {
-                      if (e0 + (ei + 1) * pb > elim) {
-                        err |= GC_DEV_TRUNCATED;
-                        ei = g.cnt;
-                        break;
+                    const uint32_t fq0 = gq - g.t0;  // the frame's first quad in the list
+                    const uint32_t ta = 4u * (ja - fq0), tb = 4u * (jb - fq0);
+                    if (e0 + g.cnt * (pb + g.wb) > elim) {
+                      err |= GC_DEV_TRUNCATED;
+                    } else {
+                      uint32_t pprev = 0;
+                      for (uint32_t x = 0; x < g.cnt; x++) {
+                        uint32_t p = eptr[e0 + x * pb];
+                        if (pb == 2) p |= (uint32_t)eptr[e0 + x * pb + 1] << 8;
+                        if (p >= 4u * g.fq || (x > 0 && p <= pprev)) {
+                          err |= GC_DEV_BAD_EXCEPTION;
+                          break;
+                        }
+                        pprev = p;
+                        if (p < ta) continue;
+                        if (p >= tb) break;
+                        const uint32_t b0 = e0 + g.cnt * pb + x * g.wb;
+                        uint32_t v = eptr[b0];
+                        if (g.wb > 1) v |= (uint32_t)eptr[b0 + 1] << 8;
+                        if (g.wb > 2) v |= ((uint32_t)eptr[b0 + 2] << 16) | ((uint32_t)eptr[b0 + 3] << 24);
+                        s_out[sw_word(min(oref + 4u * fq0 + p, kStW - 1u))] = v;
                       }
-                      uint32_t p = eptr[e0 + ei * pb];
-                      if (pb == 2) p |= (uint32_t)eptr[e0 + ei * pb + 1] << 8;
-                      if (p >= 4 * qf || (ei > 0 && p <= pprev)) {
-                        err |= GC_DEV_BAD_EXCEPTION;
-                        ei = g.cnt;
-                        break;
-                      }
-                      if (p >= t4 + 4) break;
-                      pprev = p;
-                      if (p >= t4) mask |= 1u << (p - t4);
-                      else erank++;
-                      ei++;
                     }
-                    const uint32_t wbc = g.wb == 1 ? 1u : (g.wb == 2 ? 2u : 3u);
-                    s_xinfo[loc] =
-                        mask ? (((e0 + g.cnt * pb + erank * g.wb) << 6) | (wbc << 4) | mask) : 0u;
-                    erank += __popc(mask);
                   }
-                }
-              });
+                });
+              }
             }
             S.q += a.q;
             S.d += a.d;
             S.e += a.e;
           }
-        }
-        __syncwarp();
-
-        // ---------------------------------------------------------------- unpack + d-gap scan
-        // kQPL consecutive quads per lane: shift/mask over the 4 vertical lanes, the high
-        // part of a straddling value from the current vector
-        const uint32_t nr = min(kRQ, K - u);
-        uint32_t y[4 * kQPL], opq[kQPL], cqs = 0, rsts = 0;
-        uint32_t run = 0, fl = 0;
-#pragma unroll
-        for (uint32_t s = 0; s < kQPL; s++) {
-          const uint32_t qi = kQPL * lane + s;
-          uint32_t xq[4] = {0, 0, 0, 0};
-          uint32_t op = 0, c = 0, rst = 0;
-          if (qi < nr) {
-            const uint2 dsc = s_desc[qi];
-            const uint32_t bw = dsc.y & 63u;
-            op = min((dsc.y >> 6) & 0x1FFFu, kOutWords - 4);
-            c = ((dsc.y >> 19) & 3u) + 1u;
-            rst = (dsc.y >> 21) & 1u;
-            const uint32_t m = dsc.x >> 5, off = dsc.x & 31u;
-            const bool straddle = off + bw > 32;
-            if (m < dlim && (!straddle || m + 1 < dlim)) {
-              const uint4 v0 = dptr[m];
-              const uint4 v1 = straddle ? dptr[m + 1] : make_uint4(0, 0, 0, 0);
-              const uint32_t lo = straddle ? off + bw - 32 : 0u;
-              const uint32_t mk = mask_bits(bw), ml = (1u << lo) - 1u;
-              xq[0] = (((v0.x >> off) << lo) | (v1.x & ml)) & mk;
-              xq[1] = (((v0.y >> off) << lo) | (v1.y & ml)) & mk;
-              xq[2] = (((v0.z >> off) << lo) | (v1.z & ml)) & mk;
-              xq[3] = (((v0.w >> off) << lo) | (v1.w & ml)) & mk;
-            } else {
-              err |= GC_DEV_TRUNCATED;
-            }
-            if (C::kExc) {
-              const uint32_t xi = s_xinfo[qi];
-              if (xi & 15u) {  // Group-PFD: overwrite exception slots before the scan
-                const uint32_t wb = 1u << (((xi >> 4) & 3u) - 1u);
-                const uint32_t eb0 = xi >> 6;
-                if (eb0 + __popc(xi & 15u) * wb > elim) {
-                  err |= GC_DEV_TRUNCATED;
-                } else {
-                  uint32_t r = 0;
-#pragma unroll
-                  for (int k = 0; k < 4; k++) {
-                    if (xi & (1u << k)) {
-                      const uint32_t b0 = eb0 + r * wb;
-                      uint32_t v = eptr[b0];
-                      if (wb > 1) v |= (uint32_t)eptr[b0 + 1] << 8;
-                      if (wb > 2) v |= ((uint32_t)eptr[b0 + 2] << 16) | ((uint32_t)eptr[b0 + 3] << 24);
-                      xq[k] = v;
-                      r++;
-                    }
-                  }
-                }
-              }
-            }
-          }
-          opq[s] = op;
-          cqs |= c << (3 * s);
-          rsts |= rst << s;
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            const uint32_t v = (uint32_t)k < c ? xq[k] : 0u;
-            if (DGAPS) {
-              if (k == 0 && rst) {
-                run = v;
-                fl = 1;
-              } else {
-                run += v;
-              }
-              y[4 * s + k] = run;
-            } else {
-              y[4 * s + k] = v;
-            }
-          }
-        }
-        if (DGAPS) {
-          Seg1 rt;
-          const Seg1 ex = seg1_op(rcarry, warp_excl_seg1(Seg1{fl, run}, &rt));
-          rcarry = seg1_op(rcarry, rt);
-          bool seen = false;  // values before this lane's first list start continue the prefix
-#pragma unroll
-          for (uint32_t s = 0; s < kQPL; s++) {
-            if ((rsts >> s) & 1u) seen = true;
-#pragma unroll
-            for (int k = 0; k < 4; k++)
-              if (!seen) y[4 * s + k] += ex.v;
-          }
-        }
-#pragma unroll
-        for (uint32_t s = 0; s < kQPL; s++) {
-          const uint32_t c = (cqs >> (3 * s)) & 7u;
-          const uint32_t op = opq[s];
-          if (c == 4 && (op & 3u) == 0) {
-            s_out4[sw_chunk(op >> 2)] = make_uint4(y[4 * s], y[4 * s + 1], y[4 * s + 2], y[4 * s + 3]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; k++)
-              if ((uint32_t)k < c) s_out[sw_word(op + k)] = y[4 * s + k];
-          }
-        }
-        __syncwarp();
+        };
+        if (data_st) units(std::true_type{});
+        else units(std::false_type{});
       }
     }
-    if (!waited) mbar_wait(bar, phase);
+    if (!w0done) mbar_wait(&s_bar[0], phase);
+    if (!w1done) mbar_wait(&s_bar[1], phase);
     phase ^= 1u;
+    __syncthreads();  // the tile is staged; the staging buffers and the next entries are free
+    // the next tile's copies overlap this tile's scan, look-back and stores
+    if (tid == 0) setup(tile + gridDim.x, buf ^ 1u);
 
-    // ---------------------------------------------------------------- publish + store
-    // publish the tile aggregate and store every chunk that needs no carry; the first list
-    // segment (before the tile's first list start) waits for the look-back
-    const int64_t c_lo = out_lo >> 2, c_hi = (out_hi + 3) >> 2;
-    const int64_t cb = base_int / 4;
-    const bool need_carry = DGAPS && j0 > 0;  // the tile's first quad continues a list
+    // ------------------------------------------------------------------ d-gap scan
+    const uint32_t nvalid = ok ? (last ? (uint32_t)(D.total_out - tT) : kT) : 0u;
+    const uint32_t nch = (nvalid + 3) / 4;
+    Seg1 rcarry{0u, 0u};
+    if (DGAPS && ok) {
+      // thread t scans tile positions [32t, 32t+32) (staging chunks kHalo/4 + 8t ..)
+      uint32_t v[32];
+      const uint32_t cb = kHalo / 4 + 8 * tid;
+#pragma unroll
+      for (uint32_t a = 0; a < 8; a++) {
+        const uint4 q = s_out4[sw_chunk(cb + a)];
+        v[4 * a] = q.x;
+        v[4 * a + 1] = q.y;
+        v[4 * a + 2] = q.z;
+        v[4 * a + 3] = q.w;
+      }
+      const uint32_t rb = s_rst[tid];
+      s_rst[tid] = 0u;  // clean for the next tile
+      if (rb == 0) {
+#pragma unroll
+        for (uint32_t i = 1; i < 32; i++) v[i] += v[i - 1];
+      } else {
+#pragma unroll
+        for (uint32_t i = 1; i < 32; i++) v[i] = ((rb >> i) & 1u) ? v[i] : v[i] + v[i - 1];
+      }
+      Seg1 rt;
+      const Seg1 ex = block_excl_seg1(Seg1{rb ? 1u : 0u, v[31]}, s_scr1, &rt);
+      rcarry = rt;
+      if (ex.v) {
+        const uint32_t first = rb ? (uint32_t)(__ffs(rb) - 1) : 32u;
+#pragma unroll
+        for (uint32_t i = 0; i < 32; i++)
+          if (i < first) v[i] += ex.v;
+      }
+#pragma unroll
+      for (uint32_t a = 0; a < 8; a++)
+        s_out4[sw_chunk(cb + a)] = make_uint4(v[4 * a], v[4 * a + 1], v[4 * a + 2], v[4 * a + 3]);
+      if (tid == 0)
+        st_relaxed_u64(D.tiles_b + tile, ((uint64_t)(rcarry.f ? kFlagIncl : kFlagAgg) << 32) | rcarry.v);
+      __syncthreads();
+    } else if (DGAPS && tid == 0) {
+      st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
+    }
+
+    // ------------------------------------------------------------------ stores
+    // tile chunk c = positions 4c..4c+3; positions before the first list start (reset0)
+    // get the carry of the earlier tiles
+    auto store_chunk = [&](uint32_t c, uint32_t cin, uint32_t reset0) {
+      uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
+      if (cin) {
+        const uint32_t p = 4 * c;
+        if (p < reset0) v.x += cin;
+        if (p + 1 < reset0) v.y += cin;
+        if (p + 2 < reset0) v.z += cin;
+        if (p + 3 < reset0) v.w += cin;
+      }
+      if (4 * c + 4 <= nvalid) {
+        __stcs(reinterpret_cast<uint4*>(out + tT) + c, v);
+      } else {
+        const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
+        for (uint32_t k = 0; k < 4; k++)
+          if (4 * c + k < nvalid) out[tT + 4 * c + k] = a4[k];
+      }
+    };
     if (DGAPS) {
-      reset0 = __reduce_min_sync(0xffffffffu, reset0);
-      if (lane == 0)
-        st_relaxed_u64(D.tiles_b + tile,
-                       ((uint64_t)((rcarry.f || !need_carry) ? kFlagIncl : kFlagAgg) << 32) |
-                           rcarry.v);
+      const uint32_t reset0 = s_reset0[buf];
+      const bool need_carry = ok && reset0 != 0u;  // the tile's first int continues a list
+      const uint32_t cfree = need_carry ? min(nch, (reset0 + 3u) / 4u) : 0u;
+      for (uint32_t c = cfree + tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
+      if (need_carry) {
+        if (warp == 0) {
+          const uint32_t cin = lookback_u32(D.tiles_b, tile);
+          if (tid == 0) {
+            if (!rcarry.f)
+              st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + rcarry.v));
+            s_cin = cin;
+          }
+        }
+        __syncthreads();
+        const uint32_t cin = s_cin;
+        for (uint32_t c = tid; c < cfree; c += kThreads) store_chunk(c, cin, reset0);
+      }
+    } else {
+      for (uint32_t c = tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
     }
-    const int64_t c_mid =
-        need_carry ? smin64(c_hi, smax64(c_lo, (base_int + (int64_t)reset0 + 3) >> 2)) : c_lo;
-    for (int64_t c = c_mid + lane; c < c_hi; c += 32) store_chunk(c, cb, out_lo, out_hi, 0u, 0u);
-    if (need_carry) {
-      pd_on = true;
-      pd_tile = tile;
-      pd_reset0 = reset0;
-      pd_f = rcarry.f;
-      pd_v = rcarry.v;
-      pd_lo = out_lo;
-      pd_hi = out_hi;
-      pd_clo = c_lo;
-      pd_cmid = c_mid;
-      pd_cb = cb;
-    }
-    __syncwarp();
+    __syncthreads();  // staging window, bitmap and the next tile's geometry settled
   }
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);

@@ -15,38 +15,37 @@ constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kWA = 2048;
 constexpr uint32_t kCA = kWA / kThreads;
 
-// Decode kernel (output-space warp-tiles): warp-tile t owns the quadruples that contain
-// the output positions [t*kT, (t+1)*kT).  One warp decodes one tile at a
-// time with warp-shuffle scans only; warps are persistent.
-constexpr uint32_t kT = 1024;
-constexpr uint32_t kCBW = 4;                     // control words per lane per parse round
-constexpr uint32_t kRoundWords = kCBW * 32;      // 128
-constexpr uint32_t kQPL = 9;                     // quads per lane per unpack window
-constexpr uint32_t kRQ = kQPL * 32;              // quads per unpack window (288)
-constexpr uint32_t kLT = 32;                     // lists per list round (per-warp list table)
-constexpr uint32_t kOutWords = kT + 8;           // staging window [t*kT-4, t*kT+kT+4)
-constexpr uint32_t kOutChunks = 264;             // 16-B chunks incl. swizzle slack
-constexpr uint32_t kCCap = 272;                  // staged control words (incl. halo)
-constexpr uint32_t kDCap = 288;                  // staged data vectors (4.5 KiB)
-constexpr uint32_t kECap = 768;                  // staged exception bytes
+// Decode kernel (output-space tiles): tile t owns the output ints
+// [t*kT, (t+1)*kT) exactly; it decodes every quadruple that holds one of them.
+// One CTA of kThreads threads decodes a tile; CTAs are persistent.
+constexpr uint32_t kT = 8192;                    // output ints per tile
+constexpr uint32_t kQPT = 9;                     // quads per thread per unpack round
+constexpr uint32_t kR = kQPT * kThreads;         // quad ordinals per unpack round (2304)
+constexpr uint32_t kLC = 128;                    // lists per list round (list table)
+constexpr uint32_t kUPT = 4;                     // parse units per thread per parse chunk
+constexpr uint32_t kOutW = kT + 8;               // staging ints: index = tile position + 4
+constexpr uint32_t kCCap = 1536;                 // staged control words
+constexpr uint32_t kDCap = 1600;                 // staged data vectors (25 KiB)
+constexpr uint32_t kECap = 4096;                 // staged exception bytes
 
 // Look-back flags.
 constexpr uint32_t kFlagAgg = 1, kFlagIncl = 2;
 
-struct Entry {          // tile boundary descriptor written by the index kernel (80 B)
+// Tile-start descriptor written by the index kernel (one per decode tile, 64 B): the
+// quadruple holding output int t*kT and the control word whose groups include it.
+struct Entry {
   uint32_t l;           // list of the quad containing output position t*kT
-  uint32_t j;           // its quad index within the list
-  uint32_t wq;          // raw quads of the list owned by control words before gword
-  uint32_t valid;
-  uint64_t gword;       // global control word owning the group of quad j
-  uint64_t wd;          // global data lane-bit position at the start of gword
-  uint64_t we;          // global exception byte at the start of gword
-  uint64_t dbeg;        // data lane-bit where the group of quad j starts
-  uint64_t ebeg;        // exception byte where the group of quad j starts
-  uint64_t cend;        // control words needed by the quads before (l, j): [.., cend)
-  uint64_t dend;        // data lane-bits needed by the quads before (l, j): [.., dend)
-  uint64_t eend;        // exception bytes needed by the quads before (l, j)
+  uint32_t k;           // its quad index within the list
+  uint32_t wq;          // raw quads of the list before control word w
+  uint32_t valid;       // 1 once written
+  uint64_t w;           // global control word whose groups include quad k
+  uint64_t wd;          // absolute data lane-bit at the start of w
+  uint64_t we;          // absolute exception byte at the start of w
+  uint64_t wd_end;      // ... at the end of w (bounds the previous tile's data)
+  uint64_t we_end;
+  uint64_t pad;
 };
+static_assert(sizeof(Entry) == 64, "Entry is 16 words");
 
 struct TileA {          // index-kernel look-back slot: aggregate and inclusive prefix
   uint32_t flag;        // kept in separate fields so a reader that saw flag X reads X's
@@ -134,59 +133,60 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
 
 // ---------------------------------------------------------------- scans
 // Segmented value: f = "a segment (list) starts inside"; (q, d, e) = sums since the
-// last segment start.  a (+) b = b.f ? b : (a.f, a + b).
-struct Seg3 {
-  uint32_t f, q;
-  uint64_t d, e;
+// last segment start (raw quads, data lane-bits, exception bytes; tile-relative u32).
+// a (+) b = b.f ? b : (a.f, a + b).
+struct Seg4 {
+  uint32_t f, q, d, e;
 };
-__device__ __forceinline__ Seg3 seg3_op(const Seg3& a, const Seg3& b) {
-  if (b.f) return b;
-  Seg3 r;
-  r.f = a.f;
-  r.q = a.q + b.q;
-  r.d = a.d + b.d;
-  r.e = a.e + b.e;
-  return r;
-}
-__device__ __forceinline__ Seg3 shfl_up(const Seg3& v, int delta) {
-  Seg3 r;
-  r.f = __shfl_up_sync(0xffffffffu, v.f, delta);
-  r.q = __shfl_up_sync(0xffffffffu, v.q, delta);
-  r.d = __shfl_up_sync(0xffffffffu, v.d, delta);
-  r.e = __shfl_up_sync(0xffffffffu, v.e, delta);
-  return r;
+__device__ __forceinline__ Seg4 seg4_op(const Seg4& a, const Seg4& b) {
+  return b.f ? b : Seg4{a.f, a.q + b.q, a.d + b.d, a.e + b.e};
 }
 
-// Block-wide exclusive segmented scan; returns the exclusive prefix of this thread
-// and (in *total) the block aggregate.  scratch: kWarps entries of shared memory.
-__device__ __forceinline__ Seg3 block_excl_seg3(Seg3 v, Seg3* scratch, Seg3* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Seg3 inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    Seg3 n = shfl_up(inc, o);
-    if (lane >= o) inc = seg3_op(n, inc);
+// Block-wide scans.  Each warp scans with shuffles; the kWarps warp totals are then
+// scanned by every warp at once (lane w holds warp w's total), so no thread loops over
+// the warps.  scratch: kWarps entries; two barriers (the second frees scratch).
+__device__ __forceinline__ Seg4 shfl_seg4(const Seg4& v, int src) {
+  return Seg4{__shfl_sync(0xffffffffu, v.f, src), __shfl_sync(0xffffffffu, v.q, src),
+              __shfl_sync(0xffffffffu, v.d, src), __shfl_sync(0xffffffffu, v.e, src)};
+}
+template <bool kExc>
+__device__ __forceinline__ Seg4 warp_incl_seg4(Seg4 inc, uint32_t lane, uint32_t width) {
+  for (uint32_t o = 1; o < width; o <<= 1) {
+    Seg4 n;
+    n.f = __shfl_up_sync(0xffffffffu, inc.f, o);
+    n.q = __shfl_up_sync(0xffffffffu, inc.q, o);
+    n.d = __shfl_up_sync(0xffffffffu, inc.d, o);
+    n.e = kExc ? __shfl_up_sync(0xffffffffu, inc.e, o) : 0u;
+    if (lane >= o) inc = seg4_op(n, inc);
   }
+  return inc;
+}
+// Exclusive segmented scan; returns this thread's prefix, *total = the block aggregate.
+template <bool kExc>
+__device__ __forceinline__ Seg4 block_excl_seg4(Seg4 v, Seg4* scratch, Seg4* total) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Seg4 inc = warp_incl_seg4<kExc>(v, lane, 32);
   if (lane == 31) scratch[warp] = inc;
+  Seg4 ex;
+  ex.f = __shfl_up_sync(0xffffffffu, inc.f, 1);
+  ex.q = __shfl_up_sync(0xffffffffu, inc.q, 1);
+  ex.d = __shfl_up_sync(0xffffffffu, inc.d, 1);
+  ex.e = kExc ? __shfl_up_sync(0xffffffffu, inc.e, 1) : 0u;
+  if (lane == 0) ex = Seg4{0, 0, 0, 0};
   __syncthreads();
-  Seg3 wpre = Seg3{0, 0, 0, 0};
-  Seg3 tot = Seg3{0, 0, 0, 0};
-#pragma unroll
-  for (int w = 0; w < kWarps; w++) {
-    if (w < warp) wpre = seg3_op(wpre, scratch[w]);
-    tot = seg3_op(tot, scratch[w]);
-  }
-  Seg3 ex = shfl_up(inc, 1);
-  if (lane == 0) ex = Seg3{0, 0, 0, 0};
-  *total = tot;
+  Seg4 w = lane < kWarps ? scratch[lane] : Seg4{0, 0, 0, 0};
+  w = warp_incl_seg4<kExc>(w, lane, kWarps);
+  Seg4 wpre = shfl_seg4(w, warp ? warp - 1 : 0);
+  if (warp == 0) wpre = Seg4{0, 0, 0, 0};
+  *total = shfl_seg4(w, kWarps - 1);
   __syncthreads();
-  return seg3_op(wpre, ex);
+  return seg4_op(wpre, ex);
 }
 
 // Block-wide exclusive sum of u32.
 __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* scratch,
                                                    uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -195,14 +195,14 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* scratch
   }
   if (lane == 31) scratch[warp] = inc;
   __syncthreads();
-  uint32_t wpre = 0, tot = 0;
+  uint32_t w = lane < kWarps ? scratch[lane] : 0u;
 #pragma unroll
-  for (int w = 0; w < kWarps; w++) {
-    uint32_t s = scratch[w];
-    if (w < warp) wpre += s;
-    tot += s;
+  for (uint32_t o = 1; o < kWarps; o <<= 1) {
+    uint32_t n = __shfl_up_sync(0xffffffffu, w, o);
+    if (lane >= o) w += n;
   }
-  *total = tot;
+  const uint32_t wpre = warp ? __shfl_sync(0xffffffffu, w, warp - 1) : 0u;
+  *total = __shfl_sync(0xffffffffu, w, kWarps - 1);
   __syncthreads();
   return wpre + inc - v;
 }
@@ -215,7 +215,7 @@ __device__ __forceinline__ Seg1 seg1_op(Seg1 a, Seg1 b) {
   return b.f ? b : Seg1{a.f, a.v + b.v};
 }
 __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Seg1 inc = x;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -225,19 +225,23 @@ __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* tot
     if (lane >= o) inc = seg1_op(n, inc);
   }
   if (lane == 31) scratch[warp] = inc;
-  __syncthreads();
-  Seg1 wpre{0, 0}, tot{0, 0};
-#pragma unroll
-  for (int w = 0; w < kWarps; w++) {
-    Seg1 s = scratch[w];
-    if (w < warp) wpre = seg1_op(wpre, s);
-    tot = seg1_op(tot, s);
-  }
   Seg1 ex;
   ex.f = __shfl_up_sync(0xffffffffu, inc.f, 1);
   ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
   if (lane == 0) ex = Seg1{0, 0};
-  *total = tot;
+  __syncthreads();
+  Seg1 w = lane < kWarps ? scratch[lane] : Seg1{0, 0};
+#pragma unroll
+  for (uint32_t o = 1; o < kWarps; o <<= 1) {
+    Seg1 n;
+    n.f = __shfl_up_sync(0xffffffffu, w.f, o);
+    n.v = __shfl_up_sync(0xffffffffu, w.v, o);
+    if (lane >= o) w = seg1_op(n, w);
+  }
+  Seg1 wpre{__shfl_sync(0xffffffffu, w.f, warp ? warp - 1 : 0),
+            __shfl_sync(0xffffffffu, w.v, warp ? warp - 1 : 0)};
+  if (warp == 0) wpre = Seg1{0, 0};
+  *total = Seg1{__shfl_sync(0xffffffffu, w.f, kWarps - 1), __shfl_sync(0xffffffffu, w.v, kWarps - 1)};
   __syncthreads();
   return seg1_op(wpre, ex);
 }
@@ -281,14 +285,6 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
     if (incl) return acc;
     base -= 32;
   }
-}
-
-// Staging window swizzle: 16-B chunk c is stored at chunk c ^ ((c >> 3) & 7), which
-// keeps both the blocked (16 consecutive ints per thread) and the striped (one chunk
-// per thread) 128-bit accesses free of bank conflicts.
-__device__ __forceinline__ uint32_t sw_chunk(uint32_t c) { return c ^ ((c >> 3) & 7u); }
-__device__ __forceinline__ uint32_t sw_word(uint32_t x) {
-  return (sw_chunk(x >> 2) << 2) | (x & 3u);
 }
 
 __device__ __forceinline__ uint32_t mask_bits(uint32_t b) {

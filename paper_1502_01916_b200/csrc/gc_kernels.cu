@@ -20,6 +20,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "gc.h"
 #include "gc_codecs.cuh"
@@ -46,45 +47,26 @@ struct Dev {
   TileA* tiles_a;
   uint64_t* tiles_b;
   Entry* entries;
+  uint32_t* first_list;   // [n_tiles_a] 1 + owner list of the first word of control tile a
 };
 
-// Per-thread cursor over the lists of consecutive control words.
+// Per-list view used by the group walks of the index kernel.
 struct ListCur {
-  uint64_t l;        // list index (n_lists = past the end)
-  uint64_t cw_lo;    // first control word of the list
-  uint64_t cw_hi;    // one past its last control word
+  uint64_t l;        // list index
   uint64_t n, Q;     // ints, quads
-  uint64_t oo;       // out_off
   uint64_t dbase;    // data_off * 32 (lane bits)
-  uint64_t ebase;    // exc_off
   uint64_t dlim, elim;  // data_off[l+1]*32, exc_off[l+1]
   __device__ void load(const Dev& D, uint64_t li) {
     l = li;
-    if (li >= D.n_lists) {
-      cw_lo = cw_hi = ~0ull;
-      n = Q = 0;
-      return;
-    }
-    cw_lo = D.ctrl_off[li] >> 2;
-    cw_hi = D.ctrl_off[li + 1] >> 2;
     n = D.list_n[li];
     Q = (n + 3) >> 2;
-    oo = D.out_off[li];
     dbase = D.data_off[li] * 32ull;
     dlim = D.data_off[li + 1] * 32ull;
-    ebase = D.exc_off ? D.exc_off[li] : 0ull;
     elim = D.exc_off ? D.exc_off[li + 1] : 0ull;
-  }
-  // advance to the list owning control word w (skips lists without control words)
-  __device__ void seek(const Dev& D, uint64_t w) {
-    if (l < D.n_lists && w < cw_hi) return;
-    uint64_t li = l;
-    while (li < D.n_lists && (D.ctrl_off[li + 1] >> 2) <= w) li++;
-    load(D, li);
   }
 };
 
-// Largest l in [lo, hi) with ctrl_off[l] <= key (assumes ctrl_off[lo] <= key).
+// Largest l in [lo, hi) with off[l] <= key (assumes off[lo] <= key).
 __device__ __forceinline__ uint64_t find_list(const uint64_t* off, uint64_t lo, uint64_t hi,
                                               uint64_t key) {
   uint64_t a = lo, b = hi;
@@ -103,141 +85,175 @@ __device__ __forceinline__ void report(uint32_t* s_err, uint32_t bits) {
 }
 
 // =====================================================================================
-// k_validate: directory consistency (one pass over the lists, folded into the index
-// grid).  out_off must be the exclusive scan of list_n, offsets monotone and inside the
-// streams, every non-empty list must own at least one control word.
+// k_lists: one thread per list.  Directory consistency (out_off must be the exclusive
+// scan of list_n, offsets monotone and inside the streams, every non-empty list owns at
+// least one control word) and the control-tile map: first_list[a] = 1 + the list owning
+// control word a*kWA (control areas are contiguous and 4-byte aligned).
 // =====================================================================================
-__device__ void validate_lists(const Dev& D, uint32_t tile, uint32_t* s_err) {
-  uint64_t per = (D.n_lists + D.n_tiles_a - 1) / D.n_tiles_a;
-  uint64_t l0 = (uint64_t)tile * per, l1 = mn64(D.n_lists, l0 + per);
+__global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
   uint32_t err = 0;
-  for (uint64_t l = l0 + threadIdx.x; l < l1; l += kThreads) {
-    uint64_t n = D.list_n[l];
-    uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1];
-    uint64_t d0 = D.data_off[l], d1 = D.data_off[l + 1];
-    uint64_t o0 = D.out_off[l], o1 = D.out_off[l + 1];
+  for (uint64_t l = (uint64_t)blockIdx.x * kThreads + threadIdx.x; l < D.n_lists;
+       l += (uint64_t)gridDim.x * kThreads) {
+    const uint64_t n = D.list_n[l];
+    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1];
+    const uint64_t d0 = D.data_off[l], d1 = D.data_off[l + 1];
+    const uint64_t o0 = D.out_off[l], o1 = D.out_off[l + 1];
     bool bad = (o1 != o0 + n) || (c1 < c0) || (d1 < d0) || ((c0 | c1) & 3) ||
                (c1 > 4 * D.n_ctrl_words) || (d1 > D.data_vectors) || (o1 > D.total_out) ||
                (n > 0 && c1 == c0);
     if (D.exc_off) {
-      uint64_t e0 = D.exc_off[l], e1 = D.exc_off[l + 1];
+      const uint64_t e0 = D.exc_off[l], e1 = D.exc_off[l + 1];
       bad = bad || (e1 < e0) || (e1 > D.exc_bytes);
     }
     if (l == 0) bad = bad || (o0 != 0) || (c0 != 0);
     if (l + 1 == D.n_lists) bad = bad || (o1 != D.total_out);
-    if (bad) err |= GC_DEV_TRUNCATED;
+    if (bad) {
+      err |= GC_DEV_TRUNCATED;
+      continue;
+    }
+    const uint64_t w0 = c0 >> 2, w1 = c1 >> 2;
+    for (uint64_t a = (w0 + kWA - 1) / kWA; a * kWA < w1 && a < D.n_tiles_a; a++)
+      D.first_list[a] = (uint32_t)(l + 1);
   }
-  report(s_err, err);
+  err = __reduce_or_sync(0xffffffffu, err);
+  if ((threadIdx.x & 31) == 0 && err) atomicOr(&D.hdr->status, err);
 }
 
 // =====================================================================================
 // k_index (subsystem (a)): device-wide segmented scan over the control stream.
+// Control-space tiles of kWA words, 8 per thread.  Each word is parsed on its own into
+// (raw quads, data lane-bits, exception bytes); a block scan segmented at list starts
+// plus a decoupled look-back across tiles give every word its exact position in its
+// list.  The word holding the quadruple of output int t*kT writes Entry[t]; the last
+// word of every list (and any word a cheap test finds suspicious) is walked group by
+// group to check the list's bounds and the group codes.
 // =====================================================================================
 constexpr uint32_t kLTA = kWA + 2;  // index-kernel list table entries (lists of one tile)
 
 template <class C>
 __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
-  __shared__ uint32_t s_w[kWA + 1];     // [0] = halo word (tile start - 1)
-  __shared__ uint32_t s_cw[kLTA];       // first control word of each list, relative to w0
-  __shared__ uint32_t s_q[kLTA];        // quads of each list
-  __shared__ uint32_t s_jb[kLTA];       // first quad of the list holding a tile boundary
-  __shared__ Seg3 s_scr[kWarps];
-  __shared__ Seg3 s_prefix;
-  __shared__ uint32_t s_tile, s_err, s_first_reset, s_nl, s_nq;
-  __shared__ uint64_t s_la;
-  constexpr uint32_t kQueue = 384;  // words needing a group walk (list ends, tile boundaries)
-  __shared__ uint32_t s_qw[kQueue], s_qq[kQueue];
-  __shared__ uint64_t s_qd[kQueue], s_qe[C::kExc ? kQueue : 1];
-  const int tid = threadIdx.x;
+  __shared__ uint32_t s_cw[kLTA + 1];           // first word of list la+i, relative to w0 (wraps)
+  __shared__ uint32_t s_n[kLTA];                // ints of list la+i
+  __shared__ unsigned long long s_o[kLTA];      // out_off of list la+i
+  __shared__ Seg4 s_scr[kWarps];
+  __shared__ uint32_t s_tile, s_err, s_nq, s_nl, s_nw, s_lastli, s_pq;
+  __shared__ unsigned long long s_la, s_pd, s_pe;
+  constexpr uint32_t kQueue = 384;  // words needing a group walk (list ends, suspicious words)
+  __shared__ uint32_t s_qw[kQueue], s_qi[kQueue], s_qq[kQueue];
+  __shared__ unsigned long long s_qd[kQueue], s_qe[C::kExc ? kQueue : 1];
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
     const uint32_t tile = atomicAdd(&D.hdr->counter_a, 1u);
     s_tile = tile;
     s_err = 0;
     s_nq = 0;
+    s_lastli = 0;
     const uint64_t w0 = (uint64_t)tile * kWA;
-    const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
-    // lists owning words [w0, w0+nw): la = owner of w0, lb = owner of the last word
-    uint64_t la = D.n_lists, lb = D.n_lists;
+    const uint64_t cend = D.n_lists ? mn64(D.ctrl_off[D.n_lists] >> 2, D.n_ctrl_words) : 0;
+    uint64_t nw = cend > w0 ? mn64(kWA, cend - w0) : 0;
+    uint64_t la = 0, nl = 0;
     if (nw) {
-      la = find_list(D.ctrl_off, 0, D.n_lists + 1, 4 * w0);
-      lb = find_list(D.ctrl_off, la, D.n_lists + 1, 4 * (w0 + nw - 1));
+      const uint32_t f = D.first_list[tile];
+      if (f == 0) {
+        s_err = GC_DEV_TRUNCATED;  // the directory does not cover this word
+        nw = 0;
+      } else {
+        la = f - 1;
+        uint64_t lb = D.n_lists - 1;
+        if (tile + 1 < D.n_tiles_a && D.first_list[tile + 1]) lb = D.first_list[tile + 1] - 1;
+        nl = lb >= la ? lb - la + 1 : 0;
+        if (!nl) nw = 0;
+      }
     }
     s_la = la;
-    s_nl = la < D.n_lists ? (uint32_t)(mn64(lb, D.n_lists - 1) - la + 1) : 0u;
+    s_nl = (uint32_t)mn64(nl, 0xFFFFFFFFull);
+    s_nw = (uint32_t)nw;
   }
   __syncthreads();
   const uint32_t tile = s_tile;
-  validate_lists(D, tile, &s_err);
   const uint64_t w0 = (uint64_t)tile * kWA;
-  const uint64_t nw = D.n_ctrl_words > w0 ? mn64(kWA, D.n_ctrl_words - w0) : 0;
+  const uint32_t nw = s_nw, nl = s_nl;
   const uint64_t la = s_la;
-  const uint32_t nl = s_nl;
-  for (uint32_t i = tid; i <= nw; i += kThreads) {
-    int64_t gw = (int64_t)w0 - 1 + (int64_t)i;
-    s_w[i] = (gw >= 0 && (uint64_t)gw < D.n_ctrl_words) ? D.ctrl_words[gw] : 0u;
-  }
-  for (uint32_t i = tid; i <= nl; i += kThreads) {
-    const uint64_t l = la + i;
-    s_cw[i] = (uint32_t)((D.ctrl_off[l] >> 2) - w0);  // may wrap for the first list
-    if (i < nl) {
-      const uint32_t n = D.list_n[l];
-      const uint64_t oo = D.out_off[l];
-      const uint64_t tb = (oo + kT - 1) / kT * kT;  // first tile boundary at or after oo
-      s_q[i] = (n + 3) >> 2;
-      s_jb[i] = tb < oo + n ? (uint32_t)((tb - oo) >> 2) : 0xFFFFFFFFu;
-    }
-  }
-  __syncthreads();
-
-  const uint64_t my0 = w0 + (uint64_t)tid * kCA;
-  const uint32_t myn = my0 < w0 + nw ? (uint32_t)mn64(kCA, w0 + nw - my0) : 0u;
-  uint32_t li0 = 0;
-  if (myn && nl) {
-    const uint32_t key = (uint32_t)(my0 - w0);
-    uint32_t a = 0, b = nl;
-    while (b - a > 1) {
-      const uint32_t m = (a + b) >> 1;
-      if (s_cw[m] <= key) a = m;
-      else b = m;
-    }
-    li0 = a;
-  }
-  const uint32_t mynl = nl ? myn : 0u;
-
-  // pass 1: per-word aggregates, segmented at list starts
-  Seg3 agg{0, 0, 0, 0};
-  WAgg wa_[kCA];
-  uint32_t wli[kCA];
-  {
-    uint32_t li = li0;
-    for (uint32_t k = 0; k < kCA; k++) {
-      if (k >= mynl) break;
-      const uint32_t wr = (uint32_t)(my0 + k - w0);
-      while (li + 1 < nl && s_cw[li + 1] <= wr) li++;
-      wli[k] = li;
-      const uint32_t widx = wr - s_cw[li];
-      WCtx c{s_w[wr + 1], s_w[wr], widx, s_q[li], 0u};
-      const WAgg a = word_agg<C>(c);
-      wa_[k] = a;
-      if (widx == 0) {
-        const uint64_t l = la + li;
-        agg = Seg3{1u, a.q, D.data_off[l] * 32ull + a.d, (D.exc_off ? D.exc_off[l] : 0ull) + a.e};
-      } else {
-        agg = Seg3{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
+  const bool big = nl > kLTA;  // (runs of empty lists) look the table up in global memory
+  if (!big) {
+    for (uint32_t i = tid; i <= nl && nw; i += kThreads) {
+      s_cw[i] = (uint32_t)((D.ctrl_off[la + i] >> 2) - w0);
+      if (i < nl) {
+        s_n[i] = D.list_n[la + i];
+        s_o[i] = D.out_off[la + i];
       }
     }
   }
-  if (tid == 0) s_first_reset = (mynl && s_cw[li0] == (uint32_t)(my0 - w0)) ? 1u : 0u;
-  Seg3 total;
-  Seg3 excl = block_excl_seg3(agg, s_scr, &total);
+  __syncthreads();
+  auto cw_at = [&](uint32_t i) -> uint32_t {
+    return big ? (uint32_t)((D.ctrl_off[la + i] >> 2) - w0) : s_cw[i];
+  };
+  auto n_at = [&](uint32_t i) -> uint32_t { return big ? D.list_n[la + i] : s_n[i]; };
+  auto o_at = [&](uint32_t i) -> uint64_t { return big ? D.out_off[la + i] : s_o[i]; };
 
-  // decoupled look-back across control tiles (thread 0)
+  // ---- words of this thread (8 consecutive, two 128-bit loads)
+  const uint32_t r0 = tid * kCA;
+  const uint32_t myn = r0 < nw ? min(kCA, nw - r0) : 0u;
+  uint32_t wv[kCA];
+  if (myn == kCA) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0));
+    const uint4 y = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0) + 1);
+    wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
+    wv[4] = y.x; wv[5] = y.y; wv[6] = y.z; wv[7] = y.w;
+  } else {
+#pragma unroll
+    for (uint32_t k = 0; k < kCA; k++) wv[k] = k < myn ? D.ctrl_words[w0 + r0 + k] : 0u;
+  }
+  uint32_t pw = __shfl_up_sync(0xffffffffu, wv[kCA - 1], 1);
+  if (lane == 0) pw = (C::kNeedsPrev && myn && w0 + r0 > 0) ? D.ctrl_words[w0 + r0 - 1] : 0u;
+
+  uint32_t li = 0;
+  if (myn) {  // the last table entry whose first word is <= r0 (entry 0 is the owner of w0)
+    uint32_t a = 0, b = nl;
+    while (b - a > 1) {
+      const uint32_t m = (a + b) >> 1;
+      if (cw_at(m) <= r0) a = m;
+      else b = m;
+    }
+    li = a;
+  }
+  // pass 1: per-word aggregates, segmented at list starts
+  Seg4 agg{0, 0, 0, 0};
+  WAgg wa_[kCA];
+  uint32_t wli[kCA];
+#pragma unroll
+  for (uint32_t k = 0; k < kCA; k++) {
+    wa_[k] = WAgg{0, 0, 0};
+    wli[k] = li;
+    if (k < myn) {
+      const uint32_t wr = r0 + k;
+      while (li + 1 < nl && cw_at(li + 1) <= wr) li++;
+      wli[k] = li;
+      const uint32_t widx = wr - cw_at(li);
+      const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, (n_at(li) + 3ull) >> 2, 0u};
+      const WAgg a = word_agg<C>(c);
+      wa_[k] = a;
+      agg = widx == 0 ? Seg4{1u, a.q, a.d, a.e} : Seg4{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
+    }
+  }
+  if (myn && r0 + myn == nw) s_lastli = wli[myn - 1];
+  Seg4 total;
+  const Seg4 excl = block_excl_seg4<C::kExc>(agg, s_scr, &total);
+
+  // ---- decoupled look-back across control tiles (thread 0); values are absolute
   if (tid == 0) {
     TileA* me = D.tiles_a + tile;
+    const bool first_reset = nw == 0 || cw_at(0) == 0;
+    uint64_t bd = 0, be = 0;  // absolute base of the tile's last segment (if it starts here)
     if (total.f) {
+      const uint64_t l = la + s_lastli;
+      bd = D.data_off[l] * 32ull;
+      be = D.exc_off ? D.exc_off[l] : 0ull;
+    }
+    if (total.f || nw == 0) {
       me->iq = total.q;
-      me->id = total.d;
-      me->ie = total.e;
+      me->id = bd + total.d;
+      me->ie = be + total.e;
       fence_gpu();
       st_relaxed_u32(&me->flag, kFlagIncl);
     } else {
@@ -247,131 +263,139 @@ __global__ void __launch_bounds__(kThreads) k_index(Dev D) {
       fence_gpu();
       st_relaxed_u32(&me->flag, kFlagAgg);
     }
-    Seg3 pre{0, 0, 0, 0};
-    if (!s_first_reset) {
-      int64_t p = (int64_t)tile - 1;
-      while (p >= 0) {
+    uint32_t pq = 0;
+    uint64_t pd = 0, pe = 0;
+    if (!first_reset) {
+      for (int64_t p = (int64_t)tile - 1; p >= 0; p--) {
         TileA* t = D.tiles_a + p;
         uint32_t f = ld_relaxed_u32(&t->flag);
         while (f == 0) {
-          __nanosleep(100);
+          __nanosleep(64);
           f = ld_relaxed_u32(&t->flag);
         }
         fence_gpu();
         if (f == kFlagIncl) {
-          Seg3 v{1u, ld_relaxed_u32(&t->iq), ld_relaxed_u64(&t->id), ld_relaxed_u64(&t->ie)};
-          pre = seg3_op(v, pre);
+          pq += ld_relaxed_u32(&t->iq);
+          pd += ld_relaxed_u64(&t->id);
+          pe += ld_relaxed_u64(&t->ie);
           break;
         }
-        Seg3 v{0u, ld_relaxed_u32(&t->aq), ld_relaxed_u64(&t->ad), ld_relaxed_u64(&t->ae)};
-        pre = seg3_op(v, pre);
-        p--;
+        pq += ld_relaxed_u32(&t->aq);
+        pd += ld_relaxed_u64(&t->ad);
+        pe += ld_relaxed_u64(&t->ae);
       }
       if (!total.f) {
-        Seg3 inc = seg3_op(pre, total);
-        me->iq = inc.q;
-        me->id = inc.d;
-        me->ie = inc.e;
+        me->iq = pq + total.q;
+        me->id = pd + total.d;
+        me->ie = pe + total.e;
         fence_gpu();
         st_relaxed_u32(&me->flag, kFlagIncl);
       }
     }
-    s_prefix = pre;
+    s_pq = pq;
+    s_pd = pd;
+    s_pe = pe;
   }
   __syncthreads();
 
-  // pass 2: per word, only where needed (a tile boundary falls in it, it is the list's
-  // last word, or a cheap test says it may be malformed), walk the groups: write the tile
-  // Entries and check the groups' bounds
+  // ---- pass 2: absolute positions per word; tile Entries; queue words to walk
   uint32_t err = 0;
-  auto walk_word = [&](uint64_t w, uint32_t li, const WCtx& c, const Seg3& SW) {
+  // group walk of one word: group codes, and every group of the list inside its data /
+  // exception range
+  auto walk_word = [&](uint32_t wr, uint32_t i, uint64_t q0, uint64_t d0, uint64_t e0) {
+    const uint64_t gw = w0 + wr;
+    const uint32_t w = D.ctrl_words[gw];
+    const uint32_t widx = wr - cw_at(i);
+    const uint32_t pv = (C::kNeedsPrev && widx > 0) ? D.ctrl_words[gw - 1] : 0u;
     ListCur L;
-    L.load(D, la + li);
+    L.load(D, la + i);
+    const WCtx c{w, pv, widx, L.Q, 0u};
     word_walk<C>(c, [&](const Grp& g) {
-      uint64_t gq = (uint64_t)SW.q + g.q0;
-      if (gq < L.Q && g.err) err |= g.err;
-      if (gq >= L.Q || g.nq == 0) return;
-      uint64_t ge = mn64(gq + g.nq, L.Q);
-      uint64_t gdata = SW.d + (int64_t)g.d0;
-      uint64_t gexc = SW.e + g.e0;
+      const uint64_t gq = q0 + g.q0;
+      if (gq >= L.Q) return;
+      if (g.err) err |= g.err;
+      if (g.nq == 0) return;
+      const uint64_t gdata = d0 + (int64_t)g.d0;
+      const uint64_t gexc = e0 + g.e0;
       if (gdata < L.dbase || gdata + g.dlen > L.dlim) err |= GC_DEV_TRUNCATED;
       if (C::kExc && gexc + g.elen > L.elim) err |= GC_DEV_TRUNCATED;
-      uint64_t lo_int = L.oo + 4 * gq;
-      uint64_t hi_int = L.oo + mn64(4 * ge, L.n);
-      uint64_t t = (lo_int + kT - 1) / kT;
-      if (t * kT < hi_int && t < D.n_tiles_b) {
-        uint64_t j = (t * kT - L.oo) >> 2;
-        Entry e;
-        e.l = (uint32_t)L.l;
-        e.j = (uint32_t)j;
-        e.wq = SW.q;
-        e.valid = 1;
-        e.gword = w;
-        e.wd = SW.d;
-        e.we = SW.e;
-        e.dbeg = gdata;
-        e.ebeg = gexc;
-        e.cend = w + 1;
-        if (j > gq) {  // the boundary splits a multi-quad group
-          e.dend = gdata + 32ull * (((j - gq) * g.step + 31) / 32);
-          e.eend = gexc + g.elen;
-        } else {
-          e.dend = gdata;
-          e.eend = gexc;
-        }
-        D.entries[t] = e;
-      }
     });
   };
-  Seg3 S = seg3_op(s_prefix, excl);
+  uint32_t cq = 0;
+  uint64_t cd = 0, ce = 0;
+  if (myn) {
+    if (excl.f) {  // the list of my first word started inside this tile
+      const uint64_t l = la + wli[0];
+      cq = excl.q;
+      cd = D.data_off[l] * 32ull + excl.d;
+      ce = (D.exc_off ? D.exc_off[l] : 0ull) + excl.e;
+    } else {
+      cq = s_pq + excl.q;
+      cd = s_pd + excl.d;
+      ce = s_pe + excl.e;
+    }
+  }
+#pragma unroll
   for (uint32_t k = 0; k < kCA; k++) {
-    if (k >= mynl) break;
-    const uint64_t w = my0 + k;
-    const uint32_t wr = (uint32_t)(w - w0);
-    const uint32_t li = wli[k];
-    const uint32_t widx = wr - s_cw[li];
-    const uint32_t Q = s_q[li];
-    const WCtx c{s_w[wr + 1], s_w[wr], widx, Q, 0u};
+    if (k >= myn) break;
+    const uint32_t wr = r0 + k;
+    const uint32_t i = wli[k];
+    const uint64_t l = la + i;
+    const uint32_t widx = wr - cw_at(i);
     const WAgg a = wa_[k];
     if (widx == 0) {
-      const uint64_t l = la + li;
-      S = Seg3{1u, 0u, D.data_off[l] * 32ull, D.exc_off ? D.exc_off[l] : 0ull};
+      cq = 0;
+      cd = D.data_off[l] * 32ull;
+      ce = D.exc_off ? D.exc_off[l] : 0ull;
     }
-    const Seg3 SW = S;
-    S.q += a.q;
-    S.d += a.d;
-    S.e += a.e;
-    const bool last = li + 1 < nl ? s_cw[li + 1] == wr + 1
-                                  : (uint64_t)(D.ctrl_off[la + li + 1] >> 2) == w + 1;
-    if (last && S.q < Q) err |= GC_DEV_TRUNCATED;  // the control ends before Q quads
-    const uint32_t qa = SW.q, qb = min(SW.q + a.q, Q);
-    const uint32_t jb0 = s_jb[li];
-    bool boundary = false;
-    if (qb > qa && qb > jb0) {
-      const uint32_t kk = qa > jb0 ? (qa - jb0 + (kT / 4) - 1) / (kT / 4) : 0u;
-      boundary = jb0 + kk * (kT / 4) < qb;
+    const uint32_t n = n_at(i);
+    const uint64_t Q = (n + 3ull) >> 2;
+    const uint64_t qa = cq, qb = mn64((uint64_t)cq + a.q, Q);
+    if (qb > qa) {
+      const uint64_t o = o_at(i);
+      const uint64_t lo = o + 4 * qa, hi = o + mn64(4 * qb, n);
+      const uint64_t t = (lo + kT - 1) / kT;
+      if (t * kT < hi && t < D.n_tiles_b) {
+        Entry e;
+        e.l = (uint32_t)l;
+        e.k = (uint32_t)((t * kT - o) >> 2);
+        e.wq = cq;
+        e.valid = 1;
+        e.w = w0 + wr;
+        e.wd = cd;
+        e.we = ce;
+        e.wd_end = cd + a.d;
+        e.we_end = ce + a.e;
+        e.pad = 0;
+        D.entries[t] = e;
+      }
     }
-    if (!(boundary || last || C::suspect(c))) continue;
-    // compact the words that need a group walk into a queue so the walks run lane-dense
-    const uint32_t slot = atomicAdd(&s_nq, 1u);
-    if (slot < kQueue) {
-      s_qw[slot] = wr | (li << 16);
-      s_qq[slot] = SW.q;
-      s_qd[slot] = SW.d;
-      if (C::kExc) s_qe[slot] = SW.e;
-    } else {
-      walk_word(w, li, c, SW);  // queue full: walk in place
+    const bool last = cw_at(i + 1) == wr + 1;
+    const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, Q, 0u};
+    if (last && (uint64_t)cq + a.q < Q) err |= GC_DEV_TRUNCATED;  // control ends before Q quads
+    if (last || C::suspect(c)) {
+      // compact the words that need a group walk so the walks run lane-dense
+      const uint32_t slot = atomicAdd(&s_nq, 1u);
+      if (slot < kQueue) {
+        s_qw[slot] = wr;
+        s_qi[slot] = i;
+        s_qq[slot] = cq;
+        s_qd[slot] = cd;
+        if (C::kExc) s_qe[slot] = ce;
+      } else {
+        walk_word(wr, i, cq, cd, ce);  // queue full: walk in place
+      }
     }
+    cq += a.q;
+    cd += a.d;
+    ce += a.e;
   }
   __syncthreads();
   const uint32_t nq = min(s_nq, kQueue);
-  for (uint32_t i = tid; i < nq; i += kThreads) {
-    const uint32_t wr = s_qw[i] & 0xFFFFu, li = s_qw[i] >> 16;
-    const Seg3 SW{0u, s_qq[i], s_qd[i], C::kExc ? s_qe[i] : 0ull};
-    const WCtx c{s_w[wr + 1], s_w[wr], wr - s_cw[li], s_q[li], 0u};
-    walk_word(w0 + wr, li, c, SW);
-  }
-  report(&s_err, err);
+  for (uint32_t x = tid; x < nq; x += kThreads)
+    walk_word(s_qw[x], s_qi[x], s_qq[x], s_qd[x], C::kExc ? (uint64_t)s_qe[x] : 0ull);
+  err = __reduce_or_sync(0xffffffffu, err);
+  if (lane == 0) report(&s_err, err);
   __syncthreads();
   if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
 }
@@ -432,7 +456,7 @@ namespace {
 
 struct WsLayout {
   uint64_t n_tiles_a, n_tiles_b;
-  uint64_t off_tiles_a, off_tiles_b, off_entries, bytes;
+  uint64_t off_tiles_a, off_tiles_b, off_entries, off_first, bytes;
 };
 
 WsLayout ws_layout(const gc_batch* b) {
@@ -444,7 +468,8 @@ WsLayout ws_layout(const gc_batch* b) {
   L.off_tiles_a = sizeof(WsHeader);
   L.off_tiles_b = L.off_tiles_a + L.n_tiles_a * sizeof(TileA);
   L.off_entries = L.off_tiles_b + ((L.n_tiles_b * 8 + 255) & ~255ull);
-  L.bytes = L.off_entries + L.n_tiles_b * sizeof(Entry);
+  L.off_first = L.off_entries + L.n_tiles_b * sizeof(Entry);
+  L.bytes = L.off_first + ((L.n_tiles_a * 4 + 255) & ~255ull);
   return L;
 }
 
@@ -496,35 +521,50 @@ gc_status check_device() {
   return ok ? GC_OK : GC_ERR_UNSUPPORTED_DEVICE;
 }
 
-template <class C>
-gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
-  if (stages & GC_STAGE_INDEX) {
-    k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
-    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-  }
-  if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
-  constexpr int kWPC = C::kExc ? 7 : 8;  // warps per CTA (shared memory: 2 CTAs per SM)
-  const uint32_t smem = kWPC * WarpSmem::bytes(C::kExc);
-  static bool attr_set[2] = {false, false};
+int num_sms() {
   static int n_sm = 0;
-  auto kern = dgaps ? k_decode<C, true, kWPC> : k_decode<C, false, kWPC>;
-  if (!attr_set[dgaps]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return GC_ERR_CUDA;
-    attr_set[dgaps] = true;
-  }
   if (!n_sm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 148;
   }
-  // persistent: enough CTAs to fill every SM, never more warps than tiles
-  const uint64_t want = (D.n_tiles_b + kWPC - 1) / kWPC;
-  const unsigned grid = (unsigned)mn64(want, (uint64_t)n_sm * 2);
-  kern<<<grid, 32 * kWPC, smem, st>>>(D, out);
-  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  return n_sm;
+}
+
+template <class C>
+gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
+  if (stages & GC_STAGE_INDEX) {
+    const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
+    k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)num_sms() * 8), kThreads, 0, st>>>(D);
+    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+    k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+  }
+  if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
+  const uint32_t smem = DS::bytes(C::kExc);
+  static bool attr_set[2] = {false, false};
+  static int per_sm[2] = {0, 0};
+  auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
+  if (!attr_set[dgaps]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return GC_ERR_CUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dgaps], kern, kThreads, smem) !=
+            cudaSuccess ||
+        per_sm[dgaps] < 1)
+      return GC_ERR_CUDA;
+    attr_set[dgaps] = true;
+  }
+  // tiles are assigned round-robin to a co-resident grid (the decoupled look-back waits on
+  // earlier tiles, which must all be running): a cooperative launch guarantees residency
+  const unsigned grid = (unsigned)mn64(D.n_tiles_b, (uint64_t)num_sms() * per_sm[dgaps]);
+  Dev Dv = D;
+  void* args[] = {&Dv, &out};
+  if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, st) !=
+      cudaSuccess)
+    return GC_ERR_CUDA;
+  return GC_OK;
 }
 
 gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
@@ -562,6 +602,7 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.tiles_a = (TileA*)(w + L.off_tiles_a);
   D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
   D.entries = (Entry*)(w + L.off_entries);
+  D.first_list = (uint32_t*)(w + L.off_first);
   switch (b->codec) {
     case GC_GROUP_SIMPLE:
       return launch_codec<CodecGS>(D, out, dgaps, st, stages);
