@@ -46,6 +46,21 @@ __device__ __forceinline__ uint32_t sw_word(uint32_t x) {
   return (sw_chunk(x >> 2) << 2) | (x & 3u);
 }
 
+#ifdef GC_TIMING
+#define GC_T(i)                                                         \
+  do {                                                                  \
+    if (tid == 0) {                                                     \
+      const long long now = clock64();                                  \
+      atomicAdd(&D.hdr->prof[i], (unsigned long long)(now - t_last));   \
+      t_last = now;                                                     \
+    }                                                                   \
+  } while (0)
+#else
+#define GC_T(i) \
+  do {          \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -156,6 +171,53 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
     if (dbytes) bulk_g2s(s_data, D.data + g.va, dbytes, &s_bar[1]);
   };
 
+  // A tile whose first list continues from earlier tiles publishes its aggregate and
+  // stores its carry-free chunks at once; its look-back and carry chunks wait until the
+  // next tile has parsed (just before that tile's first staging write), so the predecessors
+  // have had time to publish and the wait overlaps the next tile's list table and parse.
+  struct Pend {
+    uint32_t on, tile, nvalid, cfree, reset0, f, v, pad;
+    uint64_t tT;
+  };
+  __shared__ Pend s_pend;
+  auto flush_pending = [&]() {  // all threads; s_pend.on was read after a barrier
+    if (warp == 0) {
+      const uint32_t cin = lookback_u32(D.tiles_b, s_pend.tile, D.hdr->prof + 12);
+      if (tid == 0) {
+        if (!s_pend.f) st_relaxed_u64(D.tiles_b + s_pend.tile, ((uint64_t)kFlagIncl << 32) | (cin + s_pend.v));
+        s_cin = cin;
+      }
+    }
+    __syncthreads();
+    const uint32_t cin = s_cin, reset0 = s_pend.reset0, nvalid = s_pend.nvalid, cfree = s_pend.cfree;
+    const uint64_t tT = s_pend.tT;
+    // every thread has tested s_pend.on (before entering) and read it (above): clear it
+    // before the closing barrier, so no thread can see the stale flag afterwards
+    if (tid == 0) s_pend.on = 0;
+    for (uint32_t c = tid; c < cfree; c += kThreads) {
+      uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
+      const uint32_t p = 4 * c;
+      if (p + 4 <= reset0) {
+        v.x += cin;
+        v.y += cin;
+        v.z += cin;
+        v.w += cin;
+      } else {
+        if (p < reset0) v.x += cin;
+        if (p + 1 < reset0) v.y += cin;
+        if (p + 2 < reset0) v.z += cin;
+      }
+      if (p + 4 <= nvalid) {
+        __stcs(reinterpret_cast<uint4*>(out + tT) + c, v);
+      } else {
+        const uint32_t a4[4] = {v.x, v.y, v.z, v.w};
+        for (uint32_t k = 0; k < 4; k++)
+          if (p + k < nvalid) out[tT + p + k] = a4[k];
+      }
+    }
+    __syncthreads();
+  };
+
   // prologue: the first tile's entries and copies
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -163,13 +225,18 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
   }
   if (warp == 0) load_entries(blockIdx.x);
   if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kThreads words
-  if (tid == 0) s_reset0[0] = kT;
+  if (tid == 0) {
+    s_reset0[0] = kT;
+    s_pend.on = 0;
+  }
   __syncthreads();
   if (tid == 0) setup(blockIdx.x, 0);
   __syncthreads();
 
   uint32_t buf = 0;
+  long long t_last = clock64();
   for (uint32_t tile = blockIdx.x; tile < D.n_tiles_b; tile += gridDim.x, buf ^= 1u) {
+    GC_T(0);
     // warp 1 prefetches the next tile's entries (read after this tile's unpack)
     if (warp == 1) load_entries(tile + gridDim.x);
     if (tid == 0) s_reset0[buf ^ 1u] = kT;  // the next tile's
@@ -268,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
         w0done = true;
       }
       __syncthreads();
+      GC_T(1);
       const uint32_t rw0 = lr == 0 ? rwa : lt_cw[0];
       const uint32_t rw1 = lt_cw[cnt];
 
@@ -315,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
         Seg4 tot;
         Seg4 S = seg4_op(carry, block_excl_seg4<C::kExc>(agg, s_scr4, &tot));
         carry = seg4_op(carry, tot);
+        GC_T(2);
         if (!w1done) {
           mbar_wait(&s_bar[1], phase);
           w1done = true;
@@ -383,16 +452,20 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
             S.e += a.e;
           }
         };
+        if (DGAPS && s_pend.on) flush_pending();  // (uniform: s_pend.on only changes behind barriers)
         if (data_st) units(std::true_type{});
         else units(std::false_type{});
+        GC_T(3);
       }
     }
     if (!w0done) mbar_wait(&s_bar[0], phase);
     if (!w1done) mbar_wait(&s_bar[1], phase);
     phase ^= 1u;
+    if (DGAPS && s_pend.on) flush_pending();  // (a tile that staged nothing)
     __syncthreads();  // the tile is staged; the staging buffers and the next entries are free
     // the next tile's copies overlap this tile's scan, look-back and stores
     if (tid == 0) setup(tile + gridDim.x, buf ^ 1u);
+    GC_T(4);
 
     // ------------------------------------------------------------------ d-gap scan
     const uint32_t nvalid = ok ? (last ? (uint32_t)(D.total_out - tT) : kT) : 0u;
@@ -438,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
     }
 
+    GC_T(5);
     // ------------------------------------------------------------------ stores
     // tile chunk c = positions 4c..4c+3; positions before the first list start (reset0)
     // get the carry of the earlier tiles
@@ -463,24 +537,24 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       const bool need_carry = ok && reset0 != 0u;  // the tile's first int continues a list
       const uint32_t cfree = need_carry ? min(nch, (reset0 + 3u) / 4u) : 0u;
       for (uint32_t c = cfree + tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
-      if (need_carry) {
-        if (warp == 0) {
-          const uint32_t cin = lookback_u32(D.tiles_b, tile);
-          if (tid == 0) {
-            if (!rcarry.f)
-              st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32) | (cin + rcarry.v));
-            s_cin = cin;
-          }
-        }
-        __syncthreads();
-        const uint32_t cin = s_cin;
-        for (uint32_t c = tid; c < cfree; c += kThreads) store_chunk(c, cin, reset0);
+      if (need_carry && tid == 0) {
+        s_pend.on = 1;
+        s_pend.tile = tile;
+        s_pend.tT = tT;
+        s_pend.nvalid = nvalid;
+        s_pend.cfree = cfree;
+        s_pend.reset0 = reset0;
+        s_pend.f = rcarry.f;
+        s_pend.v = rcarry.v;
       }
+      GC_T(6);
     } else {
       for (uint32_t c = tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
     }
     __syncthreads();  // staging window, bitmap and the next tile's geometry settled
+    GC_T(7);
   }
+  if (DGAPS && s_pend.on) flush_pending();
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);
 }

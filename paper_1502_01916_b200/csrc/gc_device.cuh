@@ -59,7 +59,8 @@ struct WsHeader {
   uint32_t status;
   uint32_t counter_a;
   uint32_t counter_b;
-  uint32_t pad[61];
+  uint32_t pad[13];
+  unsigned long long prof[24];  // GC_TIMING builds: cycles per decode phase (debugging aid)
 };
 
 __host__ __device__ __forceinline__ uint64_t mn64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -252,14 +253,23 @@ __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* tot
 // including) the nearest tile that published an inclusive prefix.  Lane i watches tile
 // base-i; a window is usable as soon as every lane up to the nearest inclusive one has
 // published (the older tiles of the window are not waited for).
-__device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile) {
+__device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile,
+                                                 unsigned long long* prof = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
+#ifdef GC_TIMING
+  if (prof && lane == 0) atomicAdd(prof + 0, 1ull);
+#else
+  (void)prof;
+#endif
   uint32_t acc = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
     const int64_t idx = base - (int64_t)lane;
     uint64_t s = (uint64_t)kFlagIncl << 32;  // before tile 0: an empty inclusive prefix
     if (idx >= 0) s = ld_relaxed_u64(status + idx);
+#ifdef GC_TIMING
+    if (prof && lane == 0) atomicAdd(prof + 1, 1ull);
+#endif
     while (true) {
       const uint32_t flag = (uint32_t)(s >> 32);
       const uint32_t valid = __ballot_sync(0xffffffffu, flag != 0);
@@ -267,6 +277,17 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
       const uint32_t first = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
       const uint32_t need = first == 31u ? 0xffffffffu : ((2u << first) - 1u);
       if ((valid & need) == need) break;
+#ifdef GC_TIMING
+      if (prof) {
+        const uint32_t bad = need & ~valid;
+        if (lane == 0) {
+          atomicAdd(prof + 2, 1ull);
+          const int64_t dist = (int64_t)tile - (base - (int64_t)(__ffs(bad) - 1));
+          const int b = dist <= 1 ? 3 : dist <= 4 ? 4 : dist <= 16 ? 5 : dist <= 128 ? 6 : 7;
+          atomicAdd(prof + b, 1ull);
+        }
+      }
+#endif
       if (!(valid & (1u << lane)) && (need & (1u << lane))) {
         __nanosleep(32);
         s = ld_relaxed_u64(status + idx);
