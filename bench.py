@@ -420,7 +420,8 @@ def main():
         "per_codec": per_codec,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * len(hbs) * args.steps,
+        # per variant per step: k_lists + k_index (GC_STAGE_INDEX) and k_decode (GC_STAGE_DECODE)
+        "gpu_launches": 3 * len(hbs) * args.steps,
         "clocks": clk.summary(),
         "parity": {"verified": all_verified, "device_status": status,
                    "checksum": [int(x) for x in chk]},

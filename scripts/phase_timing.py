@@ -6,7 +6,7 @@ import torch
 import gen
 from paper_1502_01916_b200 import gc
 NAMES = ["loop top", "list table+ctrl wait", "parse+scan", "emit+unpack (+data wait)",
-         "staging barrier+setup", "d-gap scan", "carry-free stores+look-back", "carry stores+end"]
+         "staging barrier+setup", "d-gap scan", "stores", "end barrier", "deferred carry (look-back)"]
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 labels = sys.argv[2].split(",") if len(sys.argv) > 2 else ["GSC-8-B"]
 w = gen.config(cfg)
@@ -23,7 +23,7 @@ for lab in labels:
     out, ws = gc.decode_dgaps(db, out=out, ws=ws)
     torch.cuda.synchronize()
     pa = ws[64:64 + 24 * 8].cpu().numpy().view(np.uint64)
-    p = pa[:8].astype(np.float64)
+    p = pa[:9].astype(np.float64)
     print(f"   look-backs {pa[12]} windows {pa[13]} spins {pa[14]} (tiles {(hb.total_out + 8191) // 8192})"
           f"  spin distance 1:{pa[15]} 2-4:{pa[16]} 5-16:{pa[17]} 17-128:{pa[18]} >128:{pa[19]}")
 
