@@ -70,10 +70,10 @@ def config_codecs(k: int, zeta):
 
 
 def make_workload(args, rank, world):
-    import gen
-    if args.config == 5:   # config 5 is defined sharded across 8 GPUs; rank r takes shard r
-        return gen.config(5, scale=args.scale, shard=rank % 8, n_shards=8)
-    return gen.config(args.config, scale=args.scale, replica=rank)
+    """(workload, global id of its first list, scaling) of this rank (dist.shard_for_rank)."""
+    from paper_1502_01916_b200 import dist
+    sh = dist.shard_for_rank(args.config, args.scale, rank, world)
+    return sh.workload, sh.list_base, sh.scaling
 
 
 class ClockSampler:
@@ -177,7 +177,7 @@ def run_reference(args, rank, world):
     import oracle as O
     O.build()
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
-    w = make_workload(args, 0, 1)
+    w, _, scaling = make_workload(args, 0, 1)
     hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
            for c, v, f, z in config_codecs(args.config, zeta)]
     threads = len(os.sched_getaffinity(0))
@@ -195,7 +195,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "config": {"workload": w.name, "n_ints": w.n_ints,
                                         "n_lists": int(len(w.list_n)),
                                         "codecs": [gc.codec_label(c, v, f) for c, v, f, _ in
@@ -233,7 +233,7 @@ def main():
 
     # ---- inputs (untimed): generate, encode with the library's host encoder, copy to HBM
     t_setup = time.perf_counter()
-    w = make_workload(args, rank, world)
+    w, list_base, scaling = make_workload(args, rank, world)
     hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
            for c, v, f, z in codecs]
     dbs = [gc.to_device(hb, dev) for hb in hbs]
@@ -310,22 +310,10 @@ def main():
     for db, ws in zip(dbs, wss):
         docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
         status |= gc.read_device_status(ws)
-        chk += gc.checksum(db, docs, list_base=rank * len(w.list_n)).cpu().numpy().view(np.uint64)
-    if pg:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = float(t.item())
-        s = torch.tensor([int(n_ints) * len(dbs), int(status), int(bool(verified))],
-                         dtype=torch.int64, device=dev)
-        pg.all_reduce(s)
-        c = torch.from_numpy(chk.view(np.int64).copy()).to(dev)
-        pg.all_reduce(c)
-        total_ints = int(s[0].item())
-        chk = c.cpu().numpy().view(np.uint64)
-        all_verified = None if verified is None else int(s[2].item()) == world
-    else:
-        total_ints = n_ints * len(dbs)
-        all_verified = verified
+        chk += gc.checksum(db, docs, list_base=list_base).cpu().numpy().view(np.uint64)
+    from paper_1502_01916_b200 import dist as gdist
+    ms, total_ints, _, all_verified, chk = gdist.reduce_run(
+        pg, dev, ms, int(n_ints) * len(dbs), status, verified, chk)
     if rank != 0:
         if pg:
             pg.destroy_process_group()
@@ -406,11 +394,11 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": w.name, "n_ints_per_gpu": n_ints, "n_lists_per_gpu": int(len(w.list_n)),
                    "codecs": labels, "ints_per_step_all_gpus": ints_per_step_all,
-                   "parallelism": f"dp{world} (lists sharded, weak)",
+                   "parallelism": f"dp{world} (lists sharded by rank, {scaling} scaling)",
                    "l2": "no flush: every variant's working set "
                          f"({min(algo) / 1e6:.0f}-{max(algo) / 1e6:.0f} MB) exceeds the 126 MB L2",
                    "path": "gc_decode_dgaps (index scan + fused decode/d-gap scan)"},
