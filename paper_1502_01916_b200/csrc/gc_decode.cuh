@@ -42,8 +42,8 @@ struct DS {  // dynamic shared memory layout (byte offsets)
 // (8 chunks per thread) and striped (one chunk per thread) 128-bit accesses conflict-free
 // and spreads the scalar writes of thread-serial runs.
 __device__ __forceinline__ uint32_t sw_chunk(uint32_t c) { return c ^ ((c >> 3) & 7u); }
-__device__ __forceinline__ uint32_t sw_word(uint32_t x) {
-  return (sw_chunk(x >> 2) << 2) | (x & 3u);
+__device__ __forceinline__ uint32_t sw_word(uint32_t x) {  // == sw_chunk(x >> 2) * 4 + (x & 3)
+  return x ^ ((x >> 3) & 0x1Cu);
 }
 
 #ifdef GC_TIMING
