@@ -3,7 +3,7 @@
 //
 // Output-space tiles: tile t owns the output ints [t*kT, (t+1)*kT) exactly and decodes
 // every quadruple holding one of them (a quad straddling a tile edge is decoded by both
-// tiles; each keeps its own ints).  One CTA of kThreads threads decodes one tile at a
+// tiles; each keeps its own ints).  One CTA of kDT threads decodes one tile at a
 // time.  Tiles are assigned round-robin (tile = blockIdx.x + i*gridDim.x) to a
 // cooperative (co-resident) grid, so the next tile's entries and copies are known early
 // and the decoupled look-back always makes progress.  Per tile:
@@ -77,7 +77,7 @@ struct Geo {
 #define GC_DECODE_MINB 3
 #endif
 template <class C, bool DGAPS>
-__global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
+__global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS::kOut);
   uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS::kOut);
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ __align__(16) Entry s_e[2];   // entries of the next tile
   __shared__ Geo s_g[2];                   // geometry of the current / next tile
-  __shared__ Seg4 s_scr4[kWarps];
-  __shared__ Seg1 s_scr1[kWarps];
+  __shared__ Seg4 s_scr4[kDW];
+  __shared__ Seg1 s_scr1[kDW];
   __shared__ uint32_t s_reset0[2], s_cin;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
     // every thread has tested s_pend.on (before entering) and read it (above): clear it
     // before the closing barrier, so no thread can see the stale flag afterwards
     if (tid == 0) s_pend.on = 0;
-    for (uint32_t c = tid; c < cfree; c += kThreads) {
+    for (uint32_t c = tid; c < cfree; c += kDT) {
       uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
       const uint32_t p = 4 * c;
       if (p + 4 <= reset0) {
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
     mbar_init(&s_bar[1], 1);
   }
   if (warp == 0) load_entries(blockIdx.x);
-  if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kThreads words
+  if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kDT words
   if (tid == 0) {
     s_reset0[0] = kT;
     s_pend.on = 0;
@@ -343,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       constexpr uint32_t P = C::kParts;
       const uint32_t ru0 = rw0 * P, ru1 = rw1 * P;
       const uint32_t nu = ru1 > ru0 ? ru1 - ru0 : 0u;
-      const uint32_t ku = max(1u, min(kUPT, (nu + kThreads - 1) / kThreads));
+      const uint32_t ku = max(1u, min(kUPT, (nu + kDT - 1) / kDT));
       Seg4 carry = lr == 0 ? seed : Seg4{0u, 0u, 0u, 0u};
-      for (uint32_t cb0 = ru0; cb0 < ru1; cb0 += kThreads * ku) {
+      for (uint32_t cb0 = ru0; cb0 < ru1; cb0 += kDT * ku) {
         const uint32_t my0 = cb0 + tid * ku;
         const uint32_t myn = my0 < ru1 ? min(ku, ru1 - my0) : 0u;
         uint32_t li = 0;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
           }
         }
         Seg4 tot;
-        Seg4 S = seg4_op(carry, block_excl_seg4<C::kExc>(agg, s_scr4, &tot));
+        Seg4 S = seg4_op(carry, block_excl_seg4<C::kExc, kDW>(agg, s_scr4, &tot));
         carry = seg4_op(carry, tot);
         GC_T(2);
         if (!w1done) {
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
         for (uint32_t i = 1; i < 32; i++) v[i] = ((rb >> i) & 1u) ? v[i] : v[i] + v[i - 1];
       }
       Seg1 rt;
-      const Seg1 ex = block_excl_seg1(Seg1{rb ? 1u : 0u, v[31]}, s_scr1, &rt);
+      const Seg1 ex = block_excl_seg1<kDW>(Seg1{rb ? 1u : 0u, v[31]}, s_scr1, &rt);
       rcarry = rt;
       if (ex.v) {
         const uint32_t first = rb ? (uint32_t)(__ffs(rb) - 1) : 32u;
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       const uint32_t reset0 = s_reset0[buf];
       const bool need_carry = ok && reset0 != 0u;  // the tile's first int continues a list
       const uint32_t cfree = need_carry ? min(nch, (reset0 + 3u) / 4u) : 0u;
-      for (uint32_t c = cfree + tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
+      for (uint32_t c = cfree + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
       if (need_carry && tid == 0) {
         s_pend.on = 1;
         s_pend.tile = tile;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, GC_DECODE_MINB) k_decode(Dev D, uint
       }
       GC_T(6);
     } else {
-      for (uint32_t c = tid; c < nch; c += kThreads) store_chunk(c, 0u, 0u);
+      for (uint32_t c = tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
     }
     __syncthreads();  // staging window, bitmap and the next tile's geometry settled
     GC_T(7);

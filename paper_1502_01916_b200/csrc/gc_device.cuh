@@ -18,14 +18,32 @@ constexpr uint32_t kCA = kWA / kThreads;
 // Decode kernel (output-space tiles): tile t owns the output ints
 // [t*kT, (t+1)*kT) exactly; it decodes every quadruple that holds one of them.
 // One CTA of kThreads threads decodes a tile; CTAs are persistent.
-constexpr uint32_t kT = 8192;                    // output ints per tile
+#ifndef GC_T_INTS
+#define GC_T_INTS 8192
+#endif
+#ifndef GC_DT
+#define GC_DT 256
+#endif
+constexpr uint32_t kT = GC_T_INTS;               // output ints per tile
+constexpr uint32_t kDT = GC_DT;                  // decode threads per CTA (kT / 32)
+constexpr uint32_t kDW = kDT / 32;               // decode warps per CTA
+static_assert(kT == 32 * kDT, "the d-gap pass scans 32 ints per thread");
 constexpr uint32_t kQPT = 9;                     // quads per thread per unpack round
 constexpr uint32_t kR = kQPT * kThreads;         // quad ordinals per unpack round (2304)
-constexpr uint32_t kLC = 128;                    // lists per list round (list table)
+#ifndef GC_LC
+#define GC_LC 128
+#endif
+#ifndef GC_CCAP
+#define GC_CCAP 1536
+#endif
+#ifndef GC_DCAP
+#define GC_DCAP 1600
+#endif
+constexpr uint32_t kLC = GC_LC;                  // lists per list round (list table)
 constexpr uint32_t kUPT = 4;                     // parse units per thread per parse chunk
 constexpr uint32_t kOutW = kT + 8;               // staging ints: index = tile position + 4
-constexpr uint32_t kCCap = 1536;                 // staged control words
-constexpr uint32_t kDCap = 1600;                 // staged data vectors (25 KiB)
+constexpr uint32_t kCCap = GC_CCAP;              // staged control words
+constexpr uint32_t kDCap = GC_DCAP;              // staged data vectors (25 KiB)
 constexpr uint32_t kECap = 4096;                 // staged exception bytes
 
 // Look-back flags.
@@ -143,9 +161,9 @@ __device__ __forceinline__ Seg4 seg4_op(const Seg4& a, const Seg4& b) {
   return b.f ? b : Seg4{a.f, a.q + b.q, a.d + b.d, a.e + b.e};
 }
 
-// Block-wide scans.  Each warp scans with shuffles; the kWarps warp totals are then
+// Block-wide scans.  Each warp scans with shuffles; the NW warp totals are then
 // scanned by every warp at once (lane w holds warp w's total), so no thread loops over
-// the warps.  scratch: kWarps entries; two barriers (the second frees scratch).
+// the warps.  scratch: NW entries; two barriers (the second frees scratch).
 __device__ __forceinline__ Seg4 shfl_seg4(const Seg4& v, int src) {
   return Seg4{__shfl_sync(0xffffffffu, v.f, src), __shfl_sync(0xffffffffu, v.q, src),
               __shfl_sync(0xffffffffu, v.d, src), __shfl_sync(0xffffffffu, v.e, src)};
@@ -163,7 +181,7 @@ __device__ __forceinline__ Seg4 warp_incl_seg4(Seg4 inc, uint32_t lane, uint32_t
   return inc;
 }
 // Exclusive segmented scan; returns this thread's prefix, *total = the block aggregate.
-template <bool kExc>
+template <bool kExc, uint32_t NW = kWarps>
 __device__ __forceinline__ Seg4 block_excl_seg4(Seg4 v, Seg4* scratch, Seg4* total) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Seg4 inc = warp_incl_seg4<kExc>(v, lane, 32);
@@ -175,16 +193,17 @@ __device__ __forceinline__ Seg4 block_excl_seg4(Seg4 v, Seg4* scratch, Seg4* tot
   ex.e = kExc ? __shfl_up_sync(0xffffffffu, inc.e, 1) : 0u;
   if (lane == 0) ex = Seg4{0, 0, 0, 0};
   __syncthreads();
-  Seg4 w = lane < kWarps ? scratch[lane] : Seg4{0, 0, 0, 0};
-  w = warp_incl_seg4<kExc>(w, lane, kWarps);
+  Seg4 w = lane < NW ? scratch[lane] : Seg4{0, 0, 0, 0};
+  w = warp_incl_seg4<kExc>(w, lane, NW);
   Seg4 wpre = shfl_seg4(w, warp ? warp - 1 : 0);
   if (warp == 0) wpre = Seg4{0, 0, 0, 0};
-  *total = shfl_seg4(w, kWarps - 1);
+  *total = shfl_seg4(w, NW - 1);
   __syncthreads();
   return seg4_op(wpre, ex);
 }
 
 // Block-wide exclusive sum of u32.
+template <uint32_t NW = kWarps>
 __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* scratch,
                                                    uint32_t* total) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -196,14 +215,14 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* scratch
   }
   if (lane == 31) scratch[warp] = inc;
   __syncthreads();
-  uint32_t w = lane < kWarps ? scratch[lane] : 0u;
+  uint32_t w = lane < NW ? scratch[lane] : 0u;
 #pragma unroll
-  for (uint32_t o = 1; o < kWarps; o <<= 1) {
+  for (uint32_t o = 1; o < NW; o <<= 1) {
     uint32_t n = __shfl_up_sync(0xffffffffu, w, o);
     if (lane >= o) w += n;
   }
   const uint32_t wpre = warp ? __shfl_sync(0xffffffffu, w, warp - 1) : 0u;
-  *total = __shfl_sync(0xffffffffu, w, kWarps - 1);
+  *total = __shfl_sync(0xffffffffu, w, NW - 1);
   __syncthreads();
   return wpre + inc - v;
 }
@@ -215,6 +234,7 @@ struct Seg1 {
 __device__ __forceinline__ Seg1 seg1_op(Seg1 a, Seg1 b) {
   return b.f ? b : Seg1{a.f, a.v + b.v};
 }
+template <uint32_t NW = kWarps>
 __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* total) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Seg1 inc = x;
@@ -231,9 +251,9 @@ __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* tot
   ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
   if (lane == 0) ex = Seg1{0, 0};
   __syncthreads();
-  Seg1 w = lane < kWarps ? scratch[lane] : Seg1{0, 0};
+  Seg1 w = lane < NW ? scratch[lane] : Seg1{0, 0};
 #pragma unroll
-  for (uint32_t o = 1; o < kWarps; o <<= 1) {
+  for (uint32_t o = 1; o < NW; o <<= 1) {
     Seg1 n;
     n.f = __shfl_up_sync(0xffffffffu, w.f, o);
     n.v = __shfl_up_sync(0xffffffffu, w.v, o);
@@ -242,7 +262,7 @@ __device__ __forceinline__ Seg1 block_excl_seg1(Seg1 x, Seg1* scratch, Seg1* tot
   Seg1 wpre{__shfl_sync(0xffffffffu, w.f, warp ? warp - 1 : 0),
             __shfl_sync(0xffffffffu, w.v, warp ? warp - 1 : 0)};
   if (warp == 0) wpre = Seg1{0, 0};
-  *total = Seg1{__shfl_sync(0xffffffffu, w.f, kWarps - 1), __shfl_sync(0xffffffffu, w.v, kWarps - 1)};
+  *total = Seg1{__shfl_sync(0xffffffffu, w.f, NW - 1), __shfl_sync(0xffffffffu, w.v, NW - 1)};
   __syncthreads();
   return seg1_op(wpre, ex);
 }

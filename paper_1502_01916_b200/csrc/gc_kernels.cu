@@ -550,7 +550,7 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return GC_ERR_CUDA;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dgaps], kern, kThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dgaps], kern, kDT, smem) !=
             cudaSuccess ||
         per_sm[dgaps] < 1)
       return GC_ERR_CUDA;
@@ -561,7 +561,7 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   const unsigned grid = (unsigned)mn64(D.n_tiles_b, (uint64_t)num_sms() * per_sm[dgaps]);
   Dev Dv = D;
   void* args[] = {&Dv, &out};
-  if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, st) !=
+  if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kDT), args, smem, st) !=
       cudaSuccess)
     return GC_ERR_CUDA;
   return GC_OK;
