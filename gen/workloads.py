@@ -20,7 +20,9 @@ G8  Uniform[1, 2^16] inclusive; log-uniform floor(2^U), U ~ U[12,28); Bernoulli(
 """
 from __future__ import annotations
 
+import concurrent.futures
 import dataclasses
+import os
 
 import numpy as np
 
@@ -85,24 +87,79 @@ def zipf_lengths(n_lists: int, total: int, s: float, lo: int, hi: int, seed: int
     return ln[perm].astype(np.uint32)
 
 
-def _list_index(list_n: np.ndarray):
+CHUNK = 1 << 22  # elements per parallel work item
+
+
+def _threads() -> int:
+    return max(1, min(32, os.cpu_count() or 1))
+
+
+def _run(jobs):
+    """Runs the callables in `jobs` on a thread pool (numpy ufuncs release the GIL)."""
+    if len(jobs) <= 1:
+        return [j() for j in jobs]
+    with concurrent.futures.ThreadPoolExecutor(_threads()) as ex:
+        return list(ex.map(lambda j: j(), jobs))
+
+
+def _chunk_index(list_n: np.ndarray, a: int, b: int):
+    """(list id, index within list) of the elements [a, b) of the concatenated lists."""
     ln = list_n.astype(np.int64)
-    starts = np.concatenate([[0], np.cumsum(ln)[:-1]]) if len(ln) else np.zeros(0, np.int64)
-    lid = np.repeat(np.arange(len(ln), dtype=np.int64), ln)
-    idx = np.arange(int(ln.sum()), dtype=np.int64) - np.repeat(starts, ln)
-    return lid, idx, starts
+    ends = np.cumsum(ln)
+    pos = np.arange(a, b, dtype=np.int64)
+    lid = np.searchsorted(ends, pos, side="right")
+    idx = pos - (ends[lid] - ln[lid])
+    return lid, idx
+
+
+def _elementwise(list_n: np.ndarray, fn, dtype=np.uint32) -> np.ndarray:
+    """out[a:b] = fn(list id, index, a, b) over element chunks in parallel (G3 counters make
+    every element's draw independent of the chunking)."""
+    n = int(np.sum(list_n, dtype=np.int64))
+    out = np.empty(n, dtype)
+
+    def job(a, b):
+        def f():
+            lid, idx = _chunk_index(list_n, a, b)
+            out[a:b] = fn(lid, idx, a, b)
+        return f
+    _run([job(a, min(n, a + CHUNK)) for a in range(0, n, CHUNK)])
+    return out
+
+
+def _list_chunks(list_n: np.ndarray):
+    """Whole-list chunks [(first list, end list, first element, end element)] of ~CHUNK
+    elements (a list longer than CHUNK is a chunk of its own)."""
+    ends = np.cumsum(list_n.astype(np.int64))
+    out, l0, e0 = [], 0, 0
+    L = len(list_n)
+    while l0 < L:
+        l1 = int(np.searchsorted(ends, e0 + CHUNK, side="right"))
+        l1 = min(L, max(l1, l0 + 1))
+        e1 = int(ends[l1 - 1])
+        out.append((l0, l1, e0, e1))
+        l0, e0 = l1, e1
+    return out
 
 
 def uniform_subsets(list_n: np.ndarray, N: int, seed: int, list_id_base: int = 0) -> np.ndarray:
     """G5: for each list an exact uniform k-subset of [0,N), sorted (strictly increasing)."""
-    lid, idx, starts = _list_index(list_n)
-    u = uniform01(seed, 5, lid + list_id_base, idx)
-    k = np.repeat(list_n.astype(np.float64), list_n.astype(np.int64))
-    v = np.floor(u * (N - k + 1)).astype(np.uint64)
-    key = (lid.astype(np.uint64) << np.uint64(33)) | v  # lists stay contiguous after sorting
-    key.sort()
-    v = key & np.uint64((1 << 33) - 1)
-    return (v + idx.astype(np.uint64)).astype(np.uint32)
+    n = int(np.sum(list_n, dtype=np.int64))
+    out = np.empty(n, np.uint32)
+
+    def job(l0, l1, e0, e1):
+        def f():
+            lid, idx = _chunk_index(list_n, e0, e1)
+            u = uniform01(seed, 5, lid + list_id_base, idx)
+            k = list_n[lid].astype(np.float64)
+            v = np.floor(u * (N - k + 1)).astype(np.uint64)
+            key = (lid.astype(np.uint64) << np.uint64(33)) | v  # lists stay contiguous
+            key.sort()
+            v = key & np.uint64((1 << 33) - 1)
+            out[e0:e1] = (v + idx.astype(np.uint64)).astype(np.uint32)
+        return f
+    _run([job(*c) for c in _list_chunks(list_n)])
+    return out
 
 
 @dataclasses.dataclass
@@ -120,34 +177,42 @@ class Workload:
 
 
 def _gaps_cfg2(list_n, seed, base=0):
-    lid, idx, _ = _list_index(list_n)
-    lid = lid + base
-    pick = uniform01(seed, 21, lid, idx)
-    geo = geometric(uniform01(seed, 22, lid, idx), 0.05)
-    uni = 1 + np.floor(uniform01(seed, 23, lid, idx) * 65536.0).astype(np.uint64)
-    return np.where(pick < 0.7, geo, uni).astype(np.uint32)
+    def f(lid, idx, a, b):
+        lid = lid + base
+        pick = uniform01(seed, 21, lid, idx)
+        geo = geometric(uniform01(seed, 22, lid, idx), 0.05)
+        uni = 1 + np.floor(uniform01(seed, 23, lid, idx) * 65536.0).astype(np.uint64)
+        return np.where(pick < 0.7, geo, uni).astype(np.uint32)
+    return _elementwise(list_n, f)
 
 
 def _gaps_cfg3(n, seed, replica=0):
-    lid = np.full(n, replica, np.int64)
-    idx = np.arange(n, dtype=np.int64)
-    exc = uniform01(seed, 31, lid, idx) < 0.08
-    big = np.floor(2.0 ** (12.0 + 16.0 * uniform01(seed, 32, lid, idx))).astype(np.uint64)
-    geo = geometric(uniform01(seed, 33, lid, idx), 0.1)
-    return np.where(exc, big, geo).astype(np.uint32)
+    def f(lid, idx, a, b):
+        lid = np.full(b - a, replica, np.int64)
+        exc = uniform01(seed, 31, lid, idx) < 0.08
+        big = np.floor(2.0 ** (12.0 + 16.0 * uniform01(seed, 32, lid, idx))).astype(np.uint64)
+        geo = geometric(uniform01(seed, 33, lid, idx), 0.1)
+        return np.where(exc, big, geo).astype(np.uint32)
+    return _elementwise(np.array([n], np.uint32), f)
 
 
 def _gaps_cfg4(list_n, seed, base=0):
-    lid, idx, starts = _list_index(list_n)
-    lid = lid + base
-    ends = (uniform01(seed, 41, lid, idx) < 0.02).astype(np.int64)  # run ends after element
-    cs = np.cumsum(ends)
-    before_list = np.repeat(np.where(starts > 0, cs[np.maximum(starts - 1, 0)], 0),
-                            list_n.astype(np.int64)) if len(cs) else cs
-    runs_before = cs - ends - before_list     # run ends strictly before this element, in-list
-    sparse = (runs_before & 1) == 1           # runs alternate, the first run has gap 1
-    geo = geometric(uniform01(seed, 42, lid, idx), 0.001)
-    return np.where(sparse, geo, 1).astype(np.uint32)
+    # run ends after element: Bernoulli(0.02) per element (G8)
+    ends = _elementwise(list_n, lambda lid, idx, a, b:
+                        (uniform01(seed, 41, lid + base, idx) < 0.02).astype(np.uint8), np.uint8)
+    # parity of the run ends strictly before each element within its list: the inclusive
+    # XOR-scan minus this element, minus the scan before the list's first element
+    px = np.bitwise_xor.accumulate(ends) if len(ends) else ends
+    ln = list_n.astype(np.int64)
+    starts = np.cumsum(ln) - ln
+    at_start = np.where(starts > 0, px[np.maximum(starts - 1, 0)], 0).astype(np.uint8) \
+        if len(px) else np.zeros(len(ln), np.uint8)
+
+    def f(lid, idx, a, b):
+        sparse = (px[a:b] ^ ends[a:b] ^ at_start[lid]) == 1  # runs alternate, first has gap 1
+        geo = geometric(uniform01(seed, 42, lid + base, idx), 0.001)
+        return np.where(sparse, geo, 1).astype(np.uint32)
+    return _elementwise(list_n, f)
 
 
 CONFIGS = {
@@ -232,11 +297,21 @@ def checksum(list_n: np.ndarray, values: np.ndarray, list_base: int = 0):
     """G7 shard-additive checksum of decoded values (verification, not the method):
     (sum_l sum_i mix64(((l+base) << 32 | i) ^ (d_i * 0x9E3779B97F4A7C15)), sum d_i, sum n_l)
     mod 2^64, mix64 = splitmix64."""
-    lid, idx, _ = _list_index(np.asarray(list_n, np.uint32))
-    d = np.asarray(values, np.uint64)
-    with np.errstate(over="ignore"):
-        key = ((lid.astype(np.uint64) + np.uint64(list_base)) << np.uint64(32)) | idx.astype(np.uint64)
-        h = splitmix64(key ^ ((d * np.uint64(0x9E3779B97F4A7C15)) & M64))
-        H = int(np.sum(h, dtype=np.uint64))
-        S = int(np.sum(d, dtype=np.uint64))
-    return (H, S, int(np.sum(np.asarray(list_n, np.uint64))))
+    list_n = np.asarray(list_n, np.uint32)
+    values = np.asarray(values)
+    n = int(np.sum(list_n, dtype=np.int64))
+
+    def job(a, b):
+        def f():
+            lid, idx = _chunk_index(list_n, a, b)
+            d = values[a:b].astype(np.uint64)
+            with np.errstate(over="ignore"):
+                key = ((lid.astype(np.uint64) + np.uint64(list_base)) << np.uint64(32)) \
+                    | idx.astype(np.uint64)
+                h = splitmix64(key ^ ((d * np.uint64(0x9E3779B97F4A7C15)) & M64))
+                return int(np.sum(h, dtype=np.uint64)), int(np.sum(d, dtype=np.uint64))
+        return f
+    parts = _run([job(a, min(n, a + CHUNK)) for a in range(0, n, CHUNK)])
+    m = (1 << 64) - 1
+    return (sum(p[0] for p in parts) & m, sum(p[1] for p in parts) & m,
+            int(np.sum(list_n.astype(np.uint64))))

@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
 // =====================================================================================
 constexpr uint32_t kLTA = kWA + 2;  // index-kernel list table entries (lists of one tile)
 
+#ifndef GC_INDEX_MINB
+#define GC_INDEX_MINB 4
+#endif
 template <class C>
-__global__ void __launch_bounds__(kThreads) k_index(Dev D) {
+__global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   __shared__ uint32_t s_cw[kLTA + 1];           // first word of list la+i, relative to w0 (wraps)
   __shared__ uint32_t s_n[kLTA];                // ints of list la+i
   __shared__ unsigned long long s_o[kLTA];      // out_off of list la+i
