@@ -452,7 +452,11 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
             S.e += a.e;
           }
         };
-        if (DGAPS && s_pend.on) flush_pending();  // (uniform: s_pend.on only changes behind barriers)
+        if (DGAPS && s_pend.on) {  // (uniform: s_pend.on only changes behind barriers)
+          GC_T(3);
+          flush_pending();
+          GC_T(8);
+        }
         if (data_st) units(std::true_type{});
         else units(std::false_type{});
         GC_T(3);

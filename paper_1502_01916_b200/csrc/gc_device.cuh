@@ -278,6 +278,7 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
   const uint32_t lane = threadIdx.x & 31;
 #ifdef GC_TIMING
   if (prof && lane == 0) atomicAdd(prof + 0, 1ull);
+  const long long t_enter = clock64();
 #else
   (void)prof;
 #endif
@@ -323,7 +324,12 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     acc += mine;
-    if (incl) return acc;
+    if (incl) {
+#ifdef GC_TIMING
+      if (prof && lane == 0) atomicAdd(prof + 8, (unsigned long long)(clock64() - t_enter));
+#endif
+      return acc;
+    }
     base -= 32;
   }
 }

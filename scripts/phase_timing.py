@@ -28,11 +28,7 @@ for lab in labels:
           f"  spin distance 1:{pa[15]} 2-4:{pa[16]} 5-16:{pa[17]} 17-128:{pa[18]} >128:{pa[19]}")
 
     tot = p.sum()
+    print(f"   look-back cycles {100 * pa[20] / tot:.1f}% of the total")
     print(f"== {lab} cfg{cfg}: total {tot:.3e} cycles (thread 0 of every CTA, summed)")
     for n, v in zip(NAMES, p):
         print(f"   {n:22s} {100 * v / tot:5.1f}%")
-    q = pa[16:20].astype(np.float64)
-    if q.sum():
-        print(f"   k_index (thread 0 of every CTA, {q.sum():.3e} cycles):")
-        for n, v in zip(["setup+table+words", "pass 1 + block scan", "look-back", "pass 2 + walks"], q):
-            print(f"      {n:22s} {100 * v / q.sum():5.1f}%")
