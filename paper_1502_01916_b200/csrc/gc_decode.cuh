@@ -182,7 +182,11 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
   __shared__ Pend s_pend;
   auto flush_pending = [&]() {  // all threads; s_pend.on was read after a barrier
     if (warp == 0) {
+#ifdef GC_ABL_NOLB
+      const uint32_t cin = 0;
+#else
       const uint32_t cin = lookback_u32(D.tiles_b, s_pend.tile, D.hdr->prof + 12);
+#endif
       if (tid == 0) {
         if (!s_pend.f) st_relaxed_u64(D.tiles_b + s_pend.tile, ((uint64_t)kFlagIncl << 32) | (cin + s_pend.v));
         s_cin = cin;
@@ -194,7 +198,19 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     // every thread has tested s_pend.on (before entering) and read it (above): clear it
     // before the closing barrier, so no thread can see the stale flag afterwards
     if (tid == 0) s_pend.on = 0;
-    for (uint32_t c = tid; c < cfree; c += kDT) {
+    // chunks wholly before the first list start and wholly valid: the plain path
+    const uint32_t cfast = min(cfree, min(reset0, nvalid) >> 2);
+    uint4* o4 = reinterpret_cast<uint4*>(out + tT);
+#pragma unroll 2
+    for (uint32_t c = tid; c < cfast; c += kDT) {
+      uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
+      v.x += cin;
+      v.y += cin;
+      v.z += cin;
+      v.w += cin;
+      __stcs(o4 + c, v);
+    }
+    for (uint32_t c = cfast + tid; c < cfree; c += kDT) {
       uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
       const uint32_t p = 4 * c;
       if (p + 4 <= reset0) {
@@ -297,10 +313,12 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       if (rem >= 4u && (idx & 3u) == 0) {
         s_out4[sw_chunk(idx >> 2)] = make_uint4(x0, x1, x2, x3);
       } else {
+        // a list's quads sit at any word offset: four scalar stores, branch-free (the ints
+        // past the list's end go to halo words 0..2, which no tile position maps to)
         s_out[sw_word(idx)] = x0;
-        if (rem > 1u) s_out[sw_word(idx + 1)] = x1;
-        if (rem > 2u) s_out[sw_word(idx + 2)] = x2;
-        if (rem > 3u) s_out[sw_word(idx + 3)] = x3;
+        s_out[rem > 1u ? sw_word(idx + 1) : 0u] = x1;
+        s_out[rem > 2u ? sw_word(idx + 2) : 1u] = x2;
+        s_out[rem > 3u ? sw_word(idx + 3) : 2u] = x3;
       }
     };
 
@@ -500,10 +518,15 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       const Seg1 ex = block_excl_seg1<kDW>(Seg1{rb ? 1u : 0u, v[31]}, s_scr1, &rt);
       rcarry = rt;
       if (ex.v) {
-        const uint32_t first = rb ? (uint32_t)(__ffs(rb) - 1) : 32u;
+        if (rb == 0) {  // no list starts in my 32 positions (the common case)
 #pragma unroll
-        for (uint32_t i = 0; i < 32; i++)
-          if (i < first) v[i] += ex.v;
+          for (uint32_t i = 0; i < 32; i++) v[i] += ex.v;
+        } else {
+          const uint32_t first = (uint32_t)(__ffs(rb) - 1);
+#pragma unroll
+          for (uint32_t i = 0; i < 32; i++)
+            if (i < first) v[i] += ex.v;
+        }
       }
 #pragma unroll
       for (uint32_t a = 0; a < 8; a++)
@@ -536,11 +559,21 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
           if (4 * c + k < nvalid) out[tT + 4 * c + k] = a4[k];
       }
     };
+    auto store_plain = [&](uint32_t c0, uint32_t c1) {  // whole chunks, no carry
+      uint4* o4 = reinterpret_cast<uint4*>(out + tT);
+#pragma unroll 2
+      for (uint32_t c = c0 + tid; c < c1; c += kDT) __stcs(o4 + c, s_out4[sw_chunk(kHalo / 4 + c)]);
+    };
     if (DGAPS) {
       const uint32_t reset0 = s_reset0[buf];
+#ifdef GC_ABL_NOFLUSH
+      const bool need_carry = false;
+#else
       const bool need_carry = ok && reset0 != 0u;  // the tile's first int continues a list
+#endif
       const uint32_t cfree = need_carry ? min(nch, (reset0 + 3u) / 4u) : 0u;
-      for (uint32_t c = cfree + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
+      store_plain(cfree, nvalid >> 2);
+      for (uint32_t c = max(cfree, nvalid >> 2) + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
       if (need_carry && tid == 0) {
         s_pend.on = 1;
         s_pend.tile = tile;
@@ -553,7 +586,8 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       }
       GC_T(6);
     } else {
-      for (uint32_t c = tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
+      store_plain(0u, nvalid >> 2);
+      for (uint32_t c = (nvalid >> 2) + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
     }
     __syncthreads();  // staging window, bitmap and the next tile's geometry settled
     GC_T(7);

@@ -548,7 +548,11 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   const uint32_t smem = DS::bytes(C::kExc);
   static bool attr_set[2] = {false, false};
   static int per_sm[2] = {0, 0};
+#ifdef GC_ABL_NODGAP
+  auto kern = k_decode<C, false>;
+#else
   auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
+#endif
   if (!attr_set[dgaps]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
