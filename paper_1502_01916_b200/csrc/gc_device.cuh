@@ -65,13 +65,26 @@ struct Entry {
 };
 static_assert(sizeof(Entry) == 64, "Entry is 16 words");
 
-struct TileA {          // index-kernel look-back slot: aggregate and inclusive prefix
-  uint32_t flag;        // kept in separate fields so a reader that saw flag X reads X's
-  uint32_t aq;          // values, which were complete before X was published
-  uint64_t ad, ae;
-  uint32_t iq, pad;
-  uint64_t id, ie;
+// Index-kernel look-back slot of a control tile: the aggregate and the inclusive prefix,
+// each written once as two self-flagged 64-bit words (a reader needs no fence: it accepts
+// a slot when both words carry their flag).  Packing: w0 = 1<<63 | q<<31 | d[30:0],
+// w1 = 1<<63 | d[46:31]<<47 | e[46:0]  (q quads mod 2^32; d lane-bits < 2^47 and e bytes
+// < 2^47: the launch checks data_vectors < 2^42 and exc_bytes < 2^47).
+struct TileA {
+  uint64_t a0, a1;  // aggregate
+  uint64_t i0, i1;  // inclusive prefix
 };
+__device__ __forceinline__ void tilea_pack(uint32_t q, uint64_t d, uint64_t e, uint64_t& w0,
+                                           uint64_t& w1) {
+  w0 = (1ull << 63) | ((uint64_t)q << 31) | (d & 0x7FFFFFFFull);
+  w1 = (1ull << 63) | (((d >> 31) & 0xFFFFull) << 47) | (e & ((1ull << 47) - 1));
+}
+__device__ __forceinline__ void tilea_unpack(uint64_t w0, uint64_t w1, uint32_t& q, uint64_t& d,
+                                             uint64_t& e) {
+  q = (uint32_t)(w0 >> 31);
+  d = (w0 & 0x7FFFFFFFull) | (((w1 >> 47) & 0xFFFFull) << 31);
+  e = w1 & ((1ull << 47) - 1);
+}
 
 struct WsHeader {
   uint32_t status;

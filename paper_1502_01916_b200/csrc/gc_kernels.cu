@@ -243,61 +243,87 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   Seg4 total;
   const Seg4 excl = block_excl_seg4<C::kExc>(agg, s_scr, &total);
 
-  // ---- decoupled look-back across control tiles (thread 0); values are absolute
-  if (tid == 0) {
+  // ---- decoupled look-back across control tiles (warp 0, 32 predecessors per round
+  // trip); values are absolute
+  if (tid < 32) {
     TileA* me = D.tiles_a + tile;
     const bool first_reset = nw == 0 || cw_at(0) == 0;
-    uint64_t bd = 0, be = 0;  // absolute base of the tile's last segment (if it starts here)
-    if (total.f) {
-      const uint64_t l = la + s_lastli;
-      bd = D.data_off[l] * 32ull;
-      be = D.exc_off ? D.exc_off[l] : 0ull;
-    }
-    if (total.f || nw == 0) {
-      me->iq = total.q;
-      me->id = bd + total.d;
-      me->ie = be + total.e;
-      fence_gpu();
-      st_relaxed_u32(&me->flag, kFlagIncl);
-    } else {
-      me->aq = total.q;
-      me->ad = total.d;
-      me->ae = total.e;
-      fence_gpu();
-      st_relaxed_u32(&me->flag, kFlagAgg);
+    if (tid == 0) {
+      uint64_t bd = 0, be = 0;  // absolute base of the tile's last segment (if it starts here)
+      if (total.f) {
+        const uint64_t l = la + s_lastli;
+        bd = D.data_off[l] * 32ull;
+        be = D.exc_off ? D.exc_off[l] : 0ull;
+      }
+      uint64_t w0, w1;
+      if (total.f || nw == 0) {
+        tilea_pack(total.q, bd + total.d, be + total.e, w0, w1);
+        st_relaxed_u64(&me->i1, w1);
+        st_relaxed_u64(&me->i0, w0);
+      } else {
+        tilea_pack(total.q, total.d, total.e, w0, w1);
+        st_relaxed_u64(&me->a1, w1);
+        st_relaxed_u64(&me->a0, w0);
+      }
     }
     uint32_t pq = 0;
     uint64_t pd = 0, pe = 0;
     if (!first_reset) {
-      for (int64_t p = (int64_t)tile - 1; p >= 0; p--) {
-        TileA* t = D.tiles_a + p;
-        uint32_t f = ld_relaxed_u32(&t->flag);
-        while (f == 0) {
-          __nanosleep(64);
-          f = ld_relaxed_u32(&t->flag);
+      int64_t base = (int64_t)tile - 1;
+      while (true) {
+        const int64_t idx = base - (int64_t)lane;
+        const TileA* t = D.tiles_a + (idx >= 0 ? idx : 0);
+        uint64_t i0 = 1ull << 63, i1 = 1ull << 63, a0 = 0, a1 = 0;  // before tile 0: zero
+        if (idx >= 0) {
+          i0 = ld_relaxed_u64(&t->i0);
+          i1 = ld_relaxed_u64(&t->i1);
+          a0 = ld_relaxed_u64(&t->a0);
+          a1 = ld_relaxed_u64(&t->a1);
         }
-        fence_gpu();
-        if (f == kFlagIncl) {
-          pq += ld_relaxed_u32(&t->iq);
-          pd += ld_relaxed_u64(&t->id);
-          pe += ld_relaxed_u64(&t->ie);
-          break;
+        uint32_t inclm, first;
+        while (true) {
+          const bool hi = (i0 >> 63) && (i1 >> 63), ha = (a0 >> 63) && (a1 >> 63);
+          const uint32_t valid = __ballot_sync(0xffffffffu, hi || ha);
+          inclm = __ballot_sync(0xffffffffu, hi);
+          first = inclm ? (uint32_t)(__ffs(inclm) - 1) : 31u;
+          const uint32_t need = first == 31u ? 0xffffffffu : ((2u << first) - 1u);
+          if ((valid & need) == need) break;
+          if (!(valid & (1u << lane)) && (need & (1u << lane))) {
+            __nanosleep(32);
+            i0 = ld_relaxed_u64(&t->i0);
+            i1 = ld_relaxed_u64(&t->i1);
+            a0 = ld_relaxed_u64(&t->a0);
+            a1 = ld_relaxed_u64(&t->a1);
+          }
         }
-        pq += ld_relaxed_u32(&t->aq);
-        pd += ld_relaxed_u64(&t->ad);
-        pe += ld_relaxed_u64(&t->ae);
+        const bool hi = (i0 >> 63) && (i1 >> 63);
+        uint32_t q = 0;
+        uint64_t d = 0, e = 0;
+        if (lane <= first) tilea_unpack(hi ? i0 : a0, hi ? i1 : a1, q, d, e);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          q += __shfl_xor_sync(0xffffffffu, q, o);
+          d += __shfl_xor_sync(0xffffffffu, d, o);
+          e += __shfl_xor_sync(0xffffffffu, e, o);
+        }
+        pq += q;
+        pd += d;
+        pe += e;
+        if (inclm) break;
+        base -= 32;
       }
-      if (!total.f) {
-        me->iq = pq + total.q;
-        me->id = pd + total.d;
-        me->ie = pe + total.e;
-        fence_gpu();
-        st_relaxed_u32(&me->flag, kFlagIncl);
+      if (tid == 0 && !total.f) {
+        uint64_t w0, w1;
+        tilea_pack(pq + total.q, pd + total.d, pe + total.e, w0, w1);
+        st_relaxed_u64(&me->i1, w1);
+        st_relaxed_u64(&me->i0, w0);
       }
     }
-    s_pq = pq;
-    s_pd = pd;
-    s_pe = pe;
+    if (tid == 0) {
+      s_pq = pq;
+      s_pd = pd;
+      s_pe = pe;
+    }
   }
   __syncthreads();
 
@@ -506,6 +532,8 @@ gc_status check_batch(const gc_batch* b, bool device_ptrs) {
   if (b->ctrl_bytes && (!b->ctrl || !aligned16(b->ctrl))) return GC_ERR_INVALID_ARGUMENT;
   if (b->data_vectors && (!b->data || !aligned16(b->data))) return GC_ERR_INVALID_ARGUMENT;
   if (b->exc_bytes && (!b->exc || !aligned16(b->exc))) return GC_ERR_INVALID_ARGUMENT;
+  // (the index look-back packs lane-bit and exception-byte prefixes in 47 bits)
+  if (b->data_vectors >= (1ull << 42) || b->exc_bytes >= (1ull << 47)) return GC_ERR_INVALID_ARGUMENT;
   if (b->total_out && !b->n_lists) return GC_ERR_INVALID_ARGUMENT;
   if (b->total_out > (1ull << 40) || b->n_lists > 0xFFFFFFF0ull) return GC_ERR_INVALID_ARGUMENT;
   (void)device_ptrs;
