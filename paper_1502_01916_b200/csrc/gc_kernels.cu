@@ -364,24 +364,35 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
       ce = s_pe + excl.e;
     }
   }
+  // the current list's values, reloaded only when the list changes (a thread's 8 words
+  // mostly belong to one list)
+  uint32_t ci = ~0u, c_cw = 0, c_cwn = 0, c_n = 0;
+  uint64_t c_o = 0;
 #pragma unroll
   for (uint32_t k = 0; k < kCA; k++) {
     if (k >= myn) break;
     const uint32_t wr = r0 + k;
     const uint32_t i = wli[k];
     const uint64_t l = la + i;
-    const uint32_t widx = wr - cw_at(i);
+    if (i != ci) {
+      ci = i;
+      c_cw = cw_at(i);
+      c_cwn = cw_at(i + 1);
+      c_n = n_at(i);
+      c_o = o_at(i);
+    }
+    const uint32_t widx = wr - c_cw;
     const WAgg a = wa_[k];
     if (widx == 0) {
       cq = 0;
       cd = D.data_off[l] * 32ull;
       ce = D.exc_off ? D.exc_off[l] : 0ull;
     }
-    const uint32_t n = n_at(i);
+    const uint32_t n = c_n;
     const uint64_t Q = (n + 3ull) >> 2;
     const uint64_t qa = cq, qb = mn64((uint64_t)cq + a.q, Q);
     if (qb > qa) {
-      const uint64_t o = o_at(i);
+      const uint64_t o = c_o;
       const uint64_t lo = o + 4 * qa, hi = o + mn64(4 * qb, n);
       const uint64_t t = (lo + kT - 1) / kT;
       if (t * kT < hi && t < D.n_tiles_b) {
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
         D.entries[t] = e;
       }
     }
-    const bool last = cw_at(i + 1) == wr + 1;
+    const bool last = c_cwn == wr + 1;
     const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, Q, 0u};
     if (last && (uint64_t)cq + a.q < Q) err |= GC_DEV_TRUNCATED;  // control ends before Q quads
     if (last || C::suspect(c)) {
