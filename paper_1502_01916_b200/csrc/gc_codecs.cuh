@@ -14,8 +14,17 @@
 // list's quad count Q, which is how padding groups are ignored.
 #pragma once
 #include <cstdint>
+#include <type_traits>
+#include <utility>
 
 #include "gc_device.cuh"
+
+#ifndef GC_CU8_PARTS
+#define GC_CU8_PARTS 2
+#endif
+#ifndef GC_IU8_PARTS
+#define GC_IU8_PARTS 4
+#endif
 
 namespace gcd {
 
@@ -173,11 +182,26 @@ template <int CG>
 struct CodecGscCU {
   static constexpr bool kExc = false;
   static constexpr uint64_t kBackBits = 32 * CG;  // a code may start in the previous word
-  static constexpr int kParts = 1;
+  // a parse unit = the codes whose terminating 0 lies in 32/kParts control bits of a word
+  // (larger CG means shorter codes, more of them per word: split so the units stay even)
+  static constexpr int kParts = CG == 8 ? GC_CU8_PARTS : 1;
+  static constexpr uint32_t kB = 32u / kParts;  // control bits per part
   static constexpr bool kNeedsPrev = true;
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
+  // stream-order positions [0, n) of a byte-swapped word (bit 31 = first bit)
+  __device__ static __forceinline__ uint32_t top(uint32_t n) {
+    return n >= 32u ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> n);
+  }
+  __device__ static __forceinline__ uint32_t part_mask(uint32_t p) {
+    return top((p + 1u) * kB) & ~top(p * kB);
+  }
   __device__ static WAgg agg(const WCtx& c) {
+    if (kParts == 1) return WAgg{(uint32_t)__popc(~c.w), (uint32_t)(CG * 32), 0u};
+    const uint32_t z = ~__byte_perm(c.w, 0, 0x0123) & part_mask(c.part);
+    return WAgg{(uint32_t)__popc(z), (uint32_t)(CG * kB), 0u};
+  }
+  __device__ static WAgg word_agg_fast(const WCtx& c) {
     return WAgg{(uint32_t)__popc(~c.w), (uint32_t)(CG * 32), 0u};
   }
   // a run of >= 32/CG ones touching this word (stream order, previous word included)
@@ -193,19 +217,32 @@ struct CodecGscCU {
     if (have < 32u / CG) y &= y >> (32u / CG - have);
     return (uint32_t)y != 0;
   }
+  // the start (stream position relative to the word, negative: in the previous word) of
+  // the first code ending in part p; *from_prev: it begins in the previous word
+  __device__ static __forceinline__ int32_t first_start(const WCtx& c, uint32_t zs, bool& from_prev,
+                                                        bool& prev_run) {
+    const uint32_t before = zs & top(c.part * kB);
+    from_prev = false;
+    prev_run = false;
+    if (before) return 33 - (int32_t)__ffs(before);  // one bit after the last 0 before p
+    if (c.widx == 0) return 0;
+    from_prev = true;
+    const uint32_t mp = ~__byte_perm(c.prev, 0, 0x0123);
+    prev_run = mp == 0;
+    return mp ? -(int32_t)(__ffs(mp) - 1) : -32;
+  }
   template <class F>
   __device__ static __forceinline__ void emit(const WCtx& c, uint32_t q, uint32_t d, uint32_t qa,
                                               uint32_t qb, F&& f) {
-    int32_t start = 0;
-    if (c.widx > 0) {
-      const uint32_t mp = ~__byte_perm(c.prev, 0, 0x0123);
-      start = mp ? -(int32_t)(__ffs(mp) - 1) : -32;
-    }
-    uint32_t m = ~__byte_perm(c.w, 0, 0x0123);
+    const uint32_t zs = ~__byte_perm(c.w, 0, 0x0123);
+    bool fp, pr;
+    int32_t start = first_start(c, zs, fp, pr);
+    const int32_t base = (int32_t)(c.part * kB);  // d is the part's data prefix
+    uint32_t m = zs & part_mask(c.part);
     uint32_t j = q;
     while (m && j < qb) {
       const int32_t z = (int32_t)__clz(m);
-      if (j >= qa) f(j, d + (uint32_t)(CG * start), min(32u, (uint32_t)(CG * (z - start + 1))));
+      if (j >= qa) f(j, d + (uint32_t)(CG * (start - base)), min(32u, (uint32_t)(CG * (z - start + 1))));
       start = z + 1;
       m ^= 0x80000000u >> z;
       j++;
@@ -213,19 +250,12 @@ struct CodecGscCU {
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
-    uint32_t s = __byte_perm(c.w, 0, 0x0123);  // stream order: bit 31 = first bit
-    int32_t start = 0;
-    uint32_t carry_err = 0;
-    if (c.widx > 0) {
-      uint32_t mp = ~__byte_perm(c.prev, 0, 0x0123);
-      if (mp == 0) {
-        start = -32;
-        carry_err = GC_DEV_BAD_LD;  // a run of >= 32 ones
-      } else {
-        start = -(int32_t)(__ffs(mp) - 1);  // one bit after the previous word's last 0
-      }
-    }
-    uint32_t m = ~s;
+    const uint32_t zs = ~__byte_perm(c.w, 0, 0x0123);
+    bool fp, pr;
+    int32_t start = first_start(c, zs, fp, pr);
+    const int32_t base = (int32_t)(c.part * kB);
+    uint32_t carry_err = (fp && pr) ? (uint32_t)GC_DEV_BAD_LD : 0u;  // a run of >= 32 ones
+    uint32_t m = zs & part_mask(c.part);
     uint32_t q = 0;
     while (m) {
       int32_t z = (int32_t)__clz(m);
@@ -233,7 +263,7 @@ struct CodecGscCU {
       Grp g = grp0();
       g.q0 = q;
       g.nq = 1;
-      g.d0 = CG * start;
+      g.d0 = CG * (start - base);
       g.err = (u > 32u / CG) ? GC_DEV_BAD_LD : carry_err;
       g.bw = g.err ? 32u : CG * u;  // BW = CG*LD
       g.dlen = g.bw;
@@ -246,24 +276,35 @@ struct CodecGscCU {
   }
 };
 
-// ---------------------------------------------------------------- Group-Scheme, incomplete unary
-// Codes never cross a byte; the rest of a byte after its last code is 1s (P:L312,
-// A17), i.e. the byte's low-order bits in MSB-first order.
 template <int CG>
 struct CodecGscIU {
   static constexpr bool kExc = false;
   static constexpr uint64_t kBackBits = 0;
-  static constexpr int kParts = 1;
+  // a parse unit = 4/kParts control bytes (IU codes never cross a byte; CG 8 packs more,
+  // shorter codes per byte, so its words are split)
+  static constexpr int kParts = CG == 8 ? GC_IU8_PARTS : 1;
+  static constexpr int kBy = 4 / kParts;  // bytes per part
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = false;
   static constexpr bool kVectorGroups = false;
+  __device__ static __forceinline__ WAgg byte_agg(uint32_t w, int i) {
+    const uint32_t m = ~(w >> (8 * i)) & 0xFFu;
+    return WAgg{(uint32_t)__popc(m), m ? CG * (9u - (uint32_t)__ffs(m)) : 0u, 0u};  // used bits
+  }
   __device__ static WAgg agg(const WCtx& c) {
+    WAgg t{0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < kBy; i++) {
+      const WAgg a = byte_agg(c.w, (int)c.part * kBy + i);
+      t.q += a.q;
+      t.d += a.d;
+    }
+    return t;
+  }
+  __device__ static WAgg word_agg_fast(const WCtx& c) {
     uint32_t d = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t m = ~(c.w >> (8 * i)) & 0xFFu;
-      d += m ? CG * (9u - (uint32_t)__ffs(m)) : 0u;  // used bits = 8 - trailing ones
-    }
+    for (int i = 0; i < 4; i++) d += byte_agg(c.w, i).d;
     return WAgg{(uint32_t)__popc(~c.w), d, 0u};
   }
   // a byte without a 0, or a code of more than 32/CG units (padding ones excluded)
@@ -284,8 +325,8 @@ struct CodecGscIU {
                                               uint32_t qb, F&& f) {
     uint32_t j = q;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t mm = (~(c.w >> (8 * i)) & 0xFFu) << 24;
+    for (int i = 0; i < kBy; i++) {
+      uint32_t mm = (~(c.w >> (8 * ((int)c.part * kBy + i))) & 0xFFu) << 24;
       uint32_t start = 0;
       while (mm && j < qb) {
         const uint32_t z = __clz(mm);
@@ -302,8 +343,8 @@ struct CodecGscIU {
     int32_t dpos = 0;
     uint32_t q = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t m = ~(c.w >> (8 * i)) & 0xFFu;
+    for (int i = 0; i < kBy; i++) {
+      const uint32_t m = ~(c.w >> (8 * ((int)c.part * kBy + i))) & 0xFFu;
       if (m == 0) {  // 0xFF: a byte with no code
         Grp g = grp0();
         g.q0 = q;
@@ -429,9 +470,17 @@ struct CodecPFD {
   }
 };
 
+// A codec may sum a whole word faster than its parts one by one (word_agg_fast).
+template <class C, class = void>
+struct HasWordAggFast : std::false_type {};
+template <class C>
+struct HasWordAggFast<C, std::void_t<decltype(C::word_agg_fast(std::declval<const WCtx&>()))>>
+    : std::true_type {};
+
 // Whole-word helpers over a codec's kParts units (the index kernel parses whole words).
 template <class C>
 __device__ __forceinline__ WAgg word_agg(WCtx c) {
+  if constexpr (HasWordAggFast<C>::value) return C::word_agg_fast(c);
   WAgg t{0, 0, 0};
 #pragma unroll
   for (int p = 0; p < C::kParts; p++) {
