@@ -166,3 +166,36 @@ def test_api_errors():
     db.variant = 5
     with pytest.raises(gc.GcError):
         gc.decode(db)
+
+
+def test_concurrent_streams_distinct_workspaces():
+    """Calls are reentrant across distinct workspaces (include/gc.h): batches of different
+    codecs decoded on two streams at once (device and host-buffer paths, as bench.py's e2e
+    pipeline issues them) each equal the oracle."""
+    rng = np.random.default_rng(11)
+    batches = []
+    for codec, variant in [(O.GROUP_SCHEME, O.gsc_variant(8, "CU")), (O.GROUP_PFD, 0),
+                           (O.GROUP_AFOR, 0), (O.GROUP_SCHEME, O.gsc_variant(4, "IU"))]:
+        w = gen.random_lists(rng, 300, 20000, 12, 0.01)
+        hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, codec, variant))
+        batches.append((hb, O.decode_batch(hb.as_dict(), dgaps=True, threads=4)))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i, (hb, _) in enumerate(batches):
+        s = streams[i % 2]
+        with torch.cuda.stream(s):
+            db = gc.to_device(hb)
+            ws = gc.alloc_workspace(db)
+            out = torch.empty(max(hb.total_out, 4), dtype=torch.int32, device="cuda")
+        gc.decode_dgaps(db, out=out, ws=ws, stream=s)
+        host = torch.empty(max(hb.total_out, 4) * 4, dtype=torch.uint8, pin_memory=True)
+        scratch = torch.empty(gc.host_scratch_size(hb), dtype=torch.uint8, device="cuda")
+        hv = host.numpy().view(np.uint32)[:hb.total_out]
+        gc.decode_host(hb, hv, True, scratch, streams[(i + 1) % 2])
+        outs.append((db, ws, out, host, hv, scratch))
+    torch.cuda.synchronize()
+    for (hb, want), (_, ws, out, _, hv, _) in zip(batches, outs):
+        assert gc.read_device_status(ws) == 0
+        got = out[:hb.total_out].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, want)
+        assert np.array_equal(hv, want)
