@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--codecs", default="", help="comma list of labels (default: config's)")
     ap.add_argument("--pfd-zeta", default="1/10")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--side-streams", type=int, default=2)
     ap.add_argument("--sched", choices=["overlap", "serial"], default="overlap",
                     help="overlap: index stages on a side stream, concurrent with the decodes")
     ap.add_argument("--no-e2e", action="store_true")
@@ -273,7 +274,7 @@ def main():
     # per variant: index start / end, decode start / end
     ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in dbs]
           for _ in range(args.steps)]
-    side = torch.cuda.Stream(dev)
+    sides = [torch.cuda.Stream(dev) for _ in range(max(1, args.side_streams))]
 
     def step(evs=None):
         if args.sched == "serial":
@@ -291,9 +292,11 @@ def main():
         # overlap: the variants' index stages (each on its own workspace) run on a side
         # stream, ahead of and concurrently with the decodes; variant i's decode waits for
         # its own index stage only
-        side.wait_stream(stream)  # the previous step's decodes are done with the workspaces
+        for side in sides:
+            side.wait_stream(stream)  # the previous step's decodes are done with the workspaces
         done = []
         for i, (db, ws) in enumerate(zip(dbs, wss)):
+            side = sides[i % len(sides)]
             if evs is not None:
                 evs[i][0].record(side)
             gc.decode_stage(db, out, ws, True, gc.STAGE_RESET | gc.STAGE_INDEX, side)
@@ -307,7 +310,8 @@ def main():
             gc.decode_stage(db, out, ws, True, gc.STAGE_DECODE, stream)
             if evs is not None:
                 evs[i][3].record(stream)
-        stream.wait_stream(side)
+        for side in sides:
+            stream.wait_stream(side)
 
     for _ in range(args.warmup):
         step()
@@ -441,7 +445,7 @@ def main():
                    "l2": "no flush: every variant's working set "
                          f"({min(algo) / 1e6:.0f}-{max(algo) / 1e6:.0f} MB) exceeds the 126 MB L2",
                    "path": "gc_decode_dgaps (index scan + fused decode/d-gap scan)",
-                   "schedule": ("index stages on a side stream, concurrent with the decodes "
+                   "schedule": (f"index stages on {args.side_streams} side stream(s), concurrent with the decodes "
                                 "(each variant's decode waits for its own index stage; "
                                 "per-variant index_ms then includes queueing)"
                                 if args.sched == "overlap" else
