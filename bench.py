@@ -43,7 +43,7 @@ def parse_args():
     ap.add_argument("--codecs", default="", help="comma list of labels (default: config's)")
     ap.add_argument("--pfd-zeta", default="1/10")
     ap.add_argument("--no-verify", action="store_true")
-    ap.add_argument("--side-streams", type=int, default=2)
+    ap.add_argument("--side-streams", type=int, default=1)
     ap.add_argument("--sched", choices=["overlap", "serial"], default="overlap",
                     help="overlap: index stages on a side stream, concurrent with the decodes")
     ap.add_argument("--no-e2e", action="store_true")
