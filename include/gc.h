@@ -89,10 +89,11 @@ enum {
  *   ctrl, ctrl_bytes       control stream; 16-B aligned, ctrl_bytes % 16 == 0,
  *                          ctrl_bytes >= ctrl_off[n_lists]
  *   data, data_vectors     data stream of 128-bit vectors (component k of vector m
- *                          is the little-endian u32 at byte 16m+4k); 16-B aligned
+ *                          is the little-endian u32 at byte 16m+4k); 16-B aligned;
+ *                          data_vectors < 2^42 (GC_ERR_INVALID_ARGUMENT otherwise)
  *   exc, exc_bytes         Group-PFD exception stream (positions then values per
- *                          frame); 16-B aligned, exc_bytes % 16 == 0; NULL/0 for
- *                          other codecs
+ *                          frame); 16-B aligned, exc_bytes % 16 == 0, exc_bytes < 2^47;
+ *                          NULL/0 for other codecs
  *   total_out              = out_off[n_lists] = sum of list_n
  *   variant                Group-Scheme: bits 0-1 log2 CG, bits 2-3 LD kind
  *                          (0 binary, 1 complete unary, 2 incomplete unary; IU

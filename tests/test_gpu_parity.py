@@ -199,3 +199,31 @@ def test_concurrent_streams_distinct_workspaces():
         got = out[:hb.total_out].cpu().numpy().view(np.uint32)
         assert np.array_equal(got, want)
         assert np.array_equal(hv, want)
+
+
+@pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
+def test_fuzz_repeated(codec, variant):
+    """Seeded random batch shapes (list-length mixes from 1-int lists to lists spanning many
+    tiles, value widths 1-32 bits with spikes), each decoded three times on one workspace:
+    every run must equal the oracle (catches ordering races that show up only sometimes)."""
+    rng = np.random.default_rng(5000 + 16 * codec + variant)
+    for trial in range(6):
+        n_lists = int(rng.integers(1, 3000))
+        max_len = int(rng.choice([8, 300, 5000, 60000]))
+        bits = int(rng.integers(1, 33))
+        w = gen.random_lists(rng, n_lists, max_len, bits, float(rng.choice([0.0, 0.01, 0.2])))
+        if w.n_ints == 0:
+            continue
+        hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, codec, variant))
+        want = O.decode_batch(hb.as_dict(), dgaps=True, threads=4)
+        db = gc.to_device(hb)
+        ws = gc.alloc_workspace(db)
+        out = torch.empty(max(hb.total_out, 4), dtype=torch.int32, device="cuda")
+        for rep in range(3):
+            out.fill_(-1)
+            gc.decode_dgaps(db, out=out, ws=ws)
+            torch.cuda.synchronize()
+            assert gc.read_device_status(ws) == 0
+            got = out[:hb.total_out].cpu().numpy().view(np.uint32)
+            bad = np.nonzero(got != want)[0]
+            assert len(bad) == 0, f"trial {trial} rep {rep}: {len(bad)} mismatches, first {bad[:8]}"
