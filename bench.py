@@ -63,8 +63,8 @@ def config_codecs(k: int, zeta):
         return [(gc.GROUP_SIMPLE, 0, 32, zeta)]
     if k == 2:
         return [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd), 32, zeta) for cg, kd in gc.GSC_VARIANTS]
-    if k == 3:
-        return [(gc.GROUP_PFD, 0, 32, zeta)]
+    if k == 3:  # + SIMD-BP128 on the same gaps: the paper's speed leader as a control
+        return [(gc.GROUP_PFD, 0, 32, zeta), (gc.GROUP_PFD, 1, 32, zeta)]
     if k == 4:
         return [(gc.GROUP_AFOR, 0, 32, zeta)]
     return [(gc.GROUP_SIMPLE, 0, 32, zeta), (gc.GROUP_SCHEME, gc.gsc_variant(1, "CU"), 32, zeta),

@@ -48,7 +48,7 @@ typedef enum {
   GC_OK = 0,
   GC_ERR_INVALID_ARGUMENT = 1,   /* null/misaligned pointer, inconsistent sizes           */
   GC_ERR_UNKNOWN_CODEC = 2,
-  GC_ERR_BAD_VARIANT = 3,        /* Group-Scheme variant byte, or PFD frame length       */
+  GC_ERR_BAD_VARIANT = 3,        /* Group-Scheme variant byte, PFD variant / frame length */
   GC_ERR_WORKSPACE_TOO_SMALL = 4,
   GC_ERR_UNSUPPORTED_DEVICE = 5, /* not a compute-capability 10.x (sm_100a) device       */
   GC_ERR_CUDA = 6,               /* a CUDA runtime call failed (launch, copy)            */
@@ -97,7 +97,11 @@ enum {
  *   total_out              = out_off[n_lists] = sum of list_n
  *   variant                Group-Scheme: bits 0-1 log2 CG, bits 2-3 LD kind
  *                          (0 binary, 1 complete unary, 2 incomplete unary; IU
- *                          needs CG 4 or 8).  0 for other codecs.
+ *                          needs CG 4 or 8).  Group-PFD: 0, or 1 =
+ *                          SIMD-BP128 as the special case of P:L424 (frames of F
+ *                          quads packed at the width of the frame's largest int,
+ *                          no exceptions; same frame format with count 0, a frame
+ *                          with exceptions sets GC_DEV_BAD_EXCEPTION).  0 otherwise.
  *   pfd_frame_quads        Group-PFD frame length F in quadruples: 32 (default,
  *                          128 ints, u8 positions) or 128 (512 ints, u16 LE
  *                          positions).  Ignored by other codecs.
@@ -176,7 +180,8 @@ gc_status gc_decode_host(const gc_batch* host_batch, uint32_t* host_out, int dga
  *   values[sum(list_n)]  HOST, concatenated lists; docIDs when delta != 0
  *                        (each list strictly increasing; the encoder applies
  *                        the d-gap of P:L57), else the integers to store.
- *   zeta_num/zeta_den    Group-PFD exception threshold, default 1/10.
+ *   zeta_num/zeta_den    Group-PFD exception threshold, default 1/10
+ *                        (variant 1, SIMD-BP128: ignored, no exceptions).
  * gc_encode_begin encodes into encoder-owned host memory and fills the HOST
  * directory arrays ctrl_off/data_off/exc_off/out_off [n_lists+1] and
  * sizes[3] = {ctrl_bytes, data_vectors, exc_bytes} (ctrl/exc padded to 16 B).

@@ -264,6 +264,11 @@ def encode_batch(values, list_n, codec: int, variant: int = 0, delta: bool = Fal
     ln = np.ascontiguousarray(list_n, dtype=np.uint32)
     vz = v if len(v) else np.zeros(1, np.uint32)
     lz = ln if len(ln) else np.zeros(1, np.uint32)
+    if codec == GROUP_PFD and variant == 1:
+        # SIMD-BP128: each frame of 4F ints packed at "the minimum number of bits to
+        # hold the largest integer" of the frame, no exceptions -- the b rule of P:L404 with
+        # zeta = 0 (no quad may exceed b); same frame format, exception count 0
+        zeta = (0, 1)
     p = params(codec, variant, frame_quads, zeta)
     b = Batch()
     rc = lib().gco_encode_batch(C.byref(p), _u32p(vz), _u32p(lz), len(ln), int(delta), threads,

@@ -414,9 +414,12 @@ struct CodecAFOR {
 // Batch-form frame header (A31): byte 0 = b, byte 1 = wcode (0 none, 1/2/3 -> 8/16/32-bit
 // values), bytes 2-3 = exception count (LE).  Exceptions of the frame live in the
 // exception stream: count positions (u8, or u16 LE when 4F > 256) then count values.
-template <int F>
+// kE = false: SIMD-BP128 as the special case of P:L424 (PFD variant 1) -- the same frame
+// format, every frame packed at its maximum width, no exception stream.
+template <int F, bool kE = true>
 struct CodecPFD {
-  static constexpr bool kExc = true;
+  static constexpr bool kExc = kE;
+  static constexpr uint32_t kFrameQuads = F;
   static constexpr uint64_t kBackBits = 0;
   static constexpr int kParts = F / 8;        // a parse unit = 8 quads of one frame
   static constexpr bool kNeedsPrev = false;
@@ -433,13 +436,14 @@ struct CodecPFD {
     g.err = 0;
     if (b < 1 || b > 32 || wc > 3) g.err |= GC_DEV_BAD_FRAME;
     if (cnt > 4 * q || (cnt > 0 && wc == 0)) g.err |= GC_DEV_BAD_EXCEPTION;
+    if (!kE && (cnt | wc)) g.err |= GC_DEV_BAD_EXCEPTION;  // BP128 frames have none
     g.bw = (b >= 1 && b <= 32) ? b : 32u;
     g.step = g.bw;
     g.fq = q;
     g.dlen = 32u * ((q * g.bw + 31u) / 32u);   // the frame's data: fresh vectors
     g.wb = wc == 1 ? 1u : (wc == 2 ? 2u : (wc == 3 ? 4u : 0u));
-    g.cnt = g.err ? 0u : cnt;
-    g.elen = cnt * (kPosBytes + g.wb);
+    g.cnt = (g.err || !kE) ? 0u : cnt;
+    g.elen = kE ? cnt * (kPosBytes + g.wb) : 0u;
   }
   // part p covers frame quads [8p, 8p+8): 8*b data lane-bits each, the frame's padding to
   // whole vectors and all its exception bytes charged to the last / first part

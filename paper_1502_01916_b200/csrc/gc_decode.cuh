@@ -25,16 +25,31 @@
 __host__ __device__ constexpr uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
 constexpr uint32_t kHalo = 32;                     // staging index = tile position + kHalo
 constexpr uint32_t kStW = kHalo + kT + 8;          // staging ints
+// Staging capacities of a codec.  Frame codecs (PFD, SIMD-BP128) need one control word
+// per 4F ints (a tile spans <= 66), so their control staging is small and the space goes to
+// data: wide frames (up to 32 bits per int for BP128) still fit; the CTA's shared memory
+// is the same as for the other codecs.
+template <class C, class = void>
+struct Caps {
+  static constexpr uint32_t ccap = kCCap, dcap = kDCap;
+};
+template <class C>
+struct Caps<C, std::void_t<decltype(C::kFrameQuads)>> {
+  static constexpr uint32_t ccap = 256;
+  static constexpr uint32_t dcap = kDCap + (kCCap - ccap) * 4 / 16 + (C::kExc ? 0u : kECap / 16);
+};
+template <class C>
 struct DS {  // dynamic shared memory layout (byte offsets)
+  static constexpr uint32_t kCC = Caps<C>::ccap, kDC = Caps<C>::dcap;
   static constexpr uint32_t kOut = 0;                                 // kStW u32, swizzled
-  static constexpr uint32_t kData = al128(kOut + kStW * 4);           // (kDCap + 1) uint4
-  static constexpr uint32_t kCtrl = al128(kData + (kDCap + 1) * 16);  // kCCap u32
+  static constexpr uint32_t kData = al128(kOut + kStW * 4);           // (kDC + 1) uint4
+  static constexpr uint32_t kCtrl = al128(kData + (kDC + 1) * 16);    // kCC u32
   static constexpr uint32_t kLtF = 8;                                 // list table fields
-  static constexpr uint32_t kLt = al128(kCtrl + kCCap * 4);           // kLtF x (kLC + 1) u32
+  static constexpr uint32_t kLt = al128(kCtrl + kCC * 4);             // kLtF x (kLC + 1) u32
   static constexpr uint32_t kRst = al128(kLt + kLtF * (kLC + 1) * 4);  // kT/32 u32 bitmap
   static constexpr uint32_t kExcB = al128(kRst + kT / 8);             // kECap bytes (PFD)
-  __host__ __device__ static constexpr uint32_t bytes(bool exc) {
-    return exc ? al128(kExcB + kECap) : kExcB;
+  __host__ __device__ static constexpr uint32_t bytes() {
+    return C::kExc ? al128(kExcB + kECap) : kExcB;
   }
 };
 
@@ -79,13 +94,13 @@ struct Geo {
 template <class C, bool DGAPS>
 __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t sm[];
-  uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS::kOut);
-  uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS::kOut);
-  uint4* s_data = reinterpret_cast<uint4*>(sm + DS::kData);
-  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(sm + DS::kCtrl);
-  uint32_t* s_lt = reinterpret_cast<uint32_t*>(sm + DS::kLt);
-  uint32_t* s_rst = reinterpret_cast<uint32_t*>(sm + DS::kRst);
-  uint8_t* s_exc = sm + DS::kExcB;
+  uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS<C>::kOut);
+  uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS<C>::kOut);
+  uint4* s_data = reinterpret_cast<uint4*>(sm + DS<C>::kData);
+  uint32_t* s_ctrl = reinterpret_cast<uint32_t*>(sm + DS<C>::kCtrl);
+  uint32_t* s_lt = reinterpret_cast<uint32_t*>(sm + DS<C>::kLt);
+  uint32_t* s_rst = reinterpret_cast<uint32_t*>(sm + DS<C>::kRst);
+  uint8_t* s_exc = sm + DS<C>::kExcB;
   uint32_t* lt_cw = s_lt + 0 * (kLC + 1);    // first control word, relative to cbase (wraps)
   uint32_t* lt_q = s_lt + 1 * (kLC + 1);     // quads
   uint32_t* lt_n = s_lt + 2 * (kLC + 1);     // ints
@@ -141,12 +156,12 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       g.wb = wb;
       g.cbase = (wa ? wa - 1 : 0) & ~3ull;
       g.cstop = mn64((wb + 4) & ~3ull, D.n_ctrl_words);
-      g.ctrl_st = g.cstop - g.cbase <= kCCap;
+      g.ctrl_st = g.cstop - g.cbase <= DS<C>::kCC;
       // a group may start before its word's data prefix (complete unary: up to CG*32 lane
       // bits, the code's start in the previous word)
       g.va = (E0.wd - mn64(E0.wd, C::kBackBits)) >> 5;
       g.vb = mx64(g.va, mn64(last ? dend : (E1.wd_end + 31) >> 5, D.data_vectors));
-      g.data_st = g.vb - g.va <= kDCap;
+      g.data_st = g.vb - g.va <= DS<C>::kDC;
       g.ea = g.eb = 0;
       g.exc_st = 0;
       if (C::kExc) {

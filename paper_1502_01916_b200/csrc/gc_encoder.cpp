@@ -77,7 +77,14 @@ struct UnaryWriter {
 
 class ListEncoder {
  public:
-  explicit ListEncoder(const gc_encode_params& p) : p_(p) {}
+  explicit ListEncoder(const gc_encode_params& p) : p_(p) {
+    // SIMD-BP128 (PFD variant 1): b = the frame's maximum width, i.e. the PFD
+    // rule with zeta = 0 (no exceptions)
+    if (p_.codec == GC_GROUP_PFD && p_.variant == 1) {
+      p_.zeta_num = 0;
+      p_.zeta_den = 1;
+    }
+  }
 
   void encode(const uint32_t* x, uint32_t n, Buf& b) {
     const uint64_t Q = cdiv(n, 4);
@@ -323,7 +330,8 @@ bool valid_params(const gc_encode_params* p) {
       return p->variant <= 15 && kind <= 2 && !(kind == 2 && cg < 4);
     }
     case GC_GROUP_PFD:
-      return (p->pfd_frame_quads == 32 || p->pfd_frame_quads == 128) && p->zeta_den > 0;
+      return (p->pfd_frame_quads == 32 || p->pfd_frame_quads == 128) && p->variant <= 1 &&
+             (p->zeta_den > 0 || p->variant == 1);
     default:
       return false;
   }

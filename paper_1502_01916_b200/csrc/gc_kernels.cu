@@ -526,7 +526,8 @@ gc_status check_codec(const gc_batch* b) {
       return GC_OK;
     }
     case GC_GROUP_PFD:
-      return (b->pfd_frame_quads == 32 || b->pfd_frame_quads == 128) ? GC_OK : GC_ERR_BAD_VARIANT;
+      return (b->pfd_frame_quads == 32 || b->pfd_frame_quads == 128) && b->variant <= 1
+                 ? GC_OK : GC_ERR_BAD_VARIANT;
     default:
       return GC_ERR_UNKNOWN_CODEC;
   }
@@ -584,7 +585,7 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
     if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
   }
   if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
-  const uint32_t smem = DS::bytes(C::kExc);
+  const uint32_t smem = DS<C>::bytes();
   static bool attr_set[2] = {false, false};
   static int per_sm[2] = {0, 0};
 #ifdef GC_ABL_NODGAP
@@ -655,6 +656,9 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
     case GC_GROUP_AFOR:
       return launch_codec<CodecAFOR>(D, out, dgaps, st, stages);
     case GC_GROUP_PFD:
+      if (b->variant == 1)  // SIMD-BP128: no exception stream
+        return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32, false>>(D, out, dgaps, st, stages)
+                                        : launch_codec<CodecPFD<128, false>>(D, out, dgaps, st, stages);
       return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st, stages)
                                       : launch_codec<CodecPFD<128>>(D, out, dgaps, st, stages);
     default:

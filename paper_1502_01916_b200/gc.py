@@ -94,7 +94,8 @@ def codec_label(codec: int, variant: int = 0, frame_quads: int = 32) -> str:
     if codec == GROUP_SCHEME:
         return f"GSC-{1 << (variant & 3)}-{('B', 'CU', 'IU')[variant >> 2]}"
     if codec == GROUP_PFD:
-        return "G-PFD" if frame_quads == 32 else f"G-PFD-F{frame_quads}"
+        name = "BP128" if variant == 1 else "G-PFD"
+        return name if frame_quads == 32 else f"{name}-F{frame_quads}"
     return {GROUP_SIMPLE: "G-SIM", GROUP_AFOR: "G-AFOR"}[codec]
 
 

@@ -44,7 +44,7 @@ def codecs_of(k: int):
     if k == 2:
         return [(O.GROUP_SCHEME, O.gsc_variant(cg, kd)) for cg, kd in gc.GSC_VARIANTS]
     if k == 3:
-        return [(O.GROUP_PFD, 0)]
+        return [(O.GROUP_PFD, 0), (O.GROUP_PFD, 1)]
     if k == 4:
         return [(O.GROUP_AFOR, 0)]
     return [(O.GROUP_SIMPLE, 0), (O.GROUP_SCHEME, O.gsc_variant(1, "CU")),

@@ -424,3 +424,29 @@ def test_batch_dgaps_equal_generator_docids():
     assert O.decode_batch(bt, dgaps=True).tolist() == [0xFFFFFFFF, 1, 4, 1, 2, 3, 4, 5]
     assert len(bt["ctrl"]) % 16 == 0
     assert all(int(o) % 4 == 0 for o in bt["ctrl_off"])
+
+
+@pytest.mark.parametrize("F", [32, 128])
+def test_bp128_frames_at_max_width_no_exceptions(F):
+    """SIMD-BP128 as the special case of P:L424 (PFD variant 1): every frame of 4F ints is
+    packed at "the minimum number of bits to hold the largest integer among" them, with no
+    exceptions.  Checked by brute force on the headers the oracle writes: b = bit length of
+    the frame's largest int (1 for an all-zero frame), wcode = count = 0, an empty
+    exception stream, ceil(q*b/32) data vectors per frame, and the round trip."""
+    rng = np.random.default_rng(17)
+    for n, bits in ((1, 3), (4 * F - 1, 9), (4 * F, 1), (10 * 4 * F + 7, 20), (3 * 4 * F, 32)):
+        x = rng.integers(0, 1 << bits, n, dtype=np.uint64).astype(np.uint32)
+        if n > 4 * F:
+            x[4 * F:8 * F] = 0  # an all-zero frame
+        bt = O.encode_batch(x, np.array([n], np.uint32), O.GROUP_PFD, 1, frame_quads=F)
+        assert len(bt["exc"]) == 0 or not bt["exc"].any()
+        hdr = bt["ctrl"][: 4 * ((n + 4 * F - 1) // (4 * F))].reshape(-1, 4)
+        vec = 0
+        for f, h in enumerate(hdr):
+            frame = x[4 * F * f: 4 * F * (f + 1)]
+            b = max(1, int(frame.max()).bit_length())
+            assert (int(h[0]), int(h[1]), int(h[2]) | int(h[3]) << 8) == (b, 0, 0), f
+            q = (len(frame) + 3) // 4
+            vec += (q * b + 31) // 32
+        assert int(bt["data_off"][1]) == vec
+        assert np.array_equal(O.decode_batch(bt, dgaps=False), x)
