@@ -43,6 +43,8 @@ def parse_args():
     ap.add_argument("--codecs", default="", help="comma list of labels (default: config's)")
     ap.add_argument("--pfd-zeta", default="1/10")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--encode", action="store_true",
+                    help="time the GPU frame encoder (Group-PFD, SIMD-BP128) on config 3")
     ap.add_argument("--side-streams", type=int, default=1)
     ap.add_argument("--sched", choices=["overlap", "serial"], default="overlap",
                     help="overlap: index stages on a side stream, concurrent with the decodes")
@@ -210,11 +212,82 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_encode(args, dev):
+    """--encode: the GPU encoder of the frame codecs (Group-PFD, SIMD-BP128; SURVEY §8(f)
+    rank 1) on config 3's gaps resident in HBM: ints/s per codec (gc_encode_device_plan +
+    _write, events on the stream; plan reads the stream sizes back, a host sync), with the
+    oracle encoder on the host cores beside it (bounded sample)."""
+    import torch
+    import gen
+    import oracle as O
+    from paper_1502_01916_b200 import gc
+    w = gen.config(3, scale=args.scale)
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    v = torch.from_numpy(w.values.view(np.int32)).to(dev)
+    ln = torch.from_numpy(w.list_n.view(np.int32)).to(dev)
+    per, tot_ms, tot_bytes = {}, 0.0, 0
+    stream = torch.cuda.current_stream(dev)
+    for variant in (0, 1):
+        label = gc.codec_label(gc.GROUP_PFD, variant)
+        db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+        for _ in range(args.warmup):
+            db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / args.steps
+        comp = db.ctrl_bytes + 16 * db.data_vectors + db.exc_bytes
+        algo = 4 * w.n_ints + comp  # ints read + streams written
+        per[label] = {"ms": round(ms, 4), "ints_per_s": w.n_ints / (ms / 1e3),
+                      "gbs": round(algo / (ms / 1e3) / 1e9, 1),
+                      "bits_per_int": round(8 * comp / w.n_ints, 3)}
+        tot_ms += ms
+        tot_bytes += algo
+        del db
+    peak, peak_src = peaks()
+    achieved = tot_bytes / (tot_ms / 1e3) / 1e9
+    # the oracle encoder on a bounded sample of the same gaps
+    threads = len(os.sched_getaffinity(0))
+    ns = min(w.n_ints, 1 << 24)
+    t0 = time.perf_counter()
+    O.encode_batch(w.values[:ns], np.array([ns], np.uint32), O.GROUP_PFD, 0, zeta=zeta,
+                   threads=threads)
+    t_cpu = time.perf_counter() - t0
+    line = {
+        "metric": "encoded uint32 ints/sec (GPU frame encoder, Group-PFD + SIMD-BP128)",
+        "value": 2 * w.n_ints / (tot_ms / 1e3), "unit": "ints/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms,
+        "higher_is_better": True, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": w.name, "n_ints": w.n_ints, "codecs": list(per)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "bytes": "4 B per int read + the encoded streams written"},
+        "per_codec": per,
+        "cpu_baseline": {"kind": "oracle", "value": ns / t_cpu, "unit": "ints/s",
+                         "cores": threads,
+                         "sample": f"first {ns} gaps, Group-PFD, gco_encode_batch (one list, so "
+                                   "one thread does the work)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     rank, local_rank, world = dist_info()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.encode:
+        import torch
+        from paper_1502_01916_b200 import build
+        build.build()
+        torch.cuda.set_device(local_rank)
+        if rank == 0:
+            run_encode(args, torch.device("cuda", local_rank))
         return
     import torch
     from paper_1502_01916_b200 import build

@@ -203,6 +203,33 @@ gc_status gc_encode_begin(const gc_encode_params* p, const uint32_t* values,
 gc_status gc_encode_finish(void* handle, uint8_t* ctrl, void* data, uint8_t* exc);
 void gc_encode_abort(void* handle);
 
+/* ---------------------------------------------------------------------------
+ * GPU encoder of the frame codecs: Group-PFD (variant 0,
+ * P:L402-416) and SIMD-BP128 (variant 1); bytes identical to the host
+ * encoder's and the oracle's.  Other codecs: GC_ERR_UNKNOWN_CODEC (use the host
+ * encoder).  All arrays are DEVICE memory except sizes[] and the params struct.
+ *   values[total_ints], list_n[n_lists]  as for gc_encode_begin (docIDs if delta)
+ *   ws, ws_bytes         workspace of at least gc_encode_device_ws_size bytes,
+ *                        256-B aligned, owned by the caller; shared by the two calls
+ * gc_encode_device_plan fills the DEVICE directory ctrl_off/data_off/exc_off/out_off
+ * [n_lists+1] and, synchronising the stream, the HOST sizes[4] = {ctrl_bytes,
+ * data_vectors, exc_bytes (16-B padded), frames}.  The caller then allocates ctrl
+ * (4-B aligned), data (16-B aligned) and exc of those sizes, and
+ * gc_encode_device_write fills them (asynchronously, same values/ws/sizes).
+ * ------------------------------------------------------------------------- */
+gc_status gc_encode_device_ws_size(const gc_encode_params* p, uint64_t n_lists, uint64_t total_ints,
+                                   uint64_t* bytes);
+gc_status gc_encode_device_plan(const gc_encode_params* p, const uint32_t* values,
+                                const uint32_t* list_n, uint64_t n_lists, uint64_t total_ints,
+                                int delta, uint64_t* ctrl_off, uint64_t* data_off,
+                                uint64_t* exc_off, uint64_t* out_off, void* ws, uint64_t ws_bytes,
+                                uint64_t* sizes, void* stream);
+gc_status gc_encode_device_write(const gc_encode_params* p, const uint32_t* values,
+                                 const uint32_t* list_n, uint64_t n_lists, uint64_t total_ints,
+                                 int delta, const uint64_t* out_off, const uint64_t* sizes,
+                                 uint8_t* ctrl, void* data, uint8_t* exc, void* ws,
+                                 uint64_t ws_bytes, void* stream);
+
 const char* gc_status_string(gc_status s);
 int gc_abi_version(void);
 

@@ -14,7 +14,7 @@ LIB = os.path.join(PKG, "libgc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["gc_kernels.cu"]
+SOURCES_CU = ["gc_kernels.cu", "gc_encode_gpu.cu"]
 SOURCES_CPP = ["gc_encoder.cpp"]
 HEADERS = ["gc_codecs.cuh", "gc_device.cuh", "gc_decode.cuh"]
 

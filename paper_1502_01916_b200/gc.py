@@ -68,6 +68,11 @@ def _lib():
                                       P(vp)]),
             "gc_encode_finish": (i32, [vp, vp, vp, vp]),
             "gc_encode_abort": (None, [vp]),
+            "gc_encode_device_ws_size": (i32, [P(CEncodeParams), u64, u64, P(u64)]),
+            "gc_encode_device_plan": (i32, [P(CEncodeParams), vp, vp, u64, u64, i32, vp, vp, vp,
+                                            vp, vp, u64, vp, vp]),
+            "gc_encode_device_write": (i32, [P(CEncodeParams), vp, vp, u64, u64, i32, vp, vp, vp,
+                                             vp, vp, vp, u64, vp]),
             "gc_status_string": (C.c_char_p, [i32]),
             "gc_abi_version": (i32, []),
         }
@@ -215,6 +220,45 @@ def encode_batch(values: np.ndarray, list_n: np.ndarray, codec: int, variant: in
         raise GcError(st, "gc_encode_finish")
     return HostBatch(codec, variant, frame_quads, ln.copy(), offs[0], offs[1], offs[2], offs[3],
                      ctrl, data, exc)
+
+
+def encode_device(values, list_n, codec: int = GROUP_PFD, variant: int = 0, delta: bool = False,
+                  frame_quads: int = 32, zeta=(1, 10), stream=None, ws=None) -> DeviceBatch:
+    """GPU encoder of the frame codecs (gc_encode_device_plan/write): Group-PFD (variant 0)
+    and SIMD-BP128 (variant 1).  values, list_n: int32/uint32 CUDA tensors.  Returns the
+    batch resident on the device, ready for decode()."""
+    import torch
+    dev = values.device
+    L, N = int(list_n.numel()), int(values.numel())
+    prm = CEncodeParams(codec, variant, frame_quads, zeta[0], zeta[1])
+    need = C.c_uint64()
+    st = _lib().gc_encode_device_ws_size(C.byref(prm), L, N, C.byref(need))
+    if st:
+        raise GcError(st, "gc_encode_device_ws_size")
+    if ws is None or ws.numel() < need.value:
+        ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+    offs = [torch.zeros(L + 1, dtype=torch.int64, device=dev) for _ in range(4)]
+    sizes = np.zeros(4, np.uint64)
+    sp = _stream_ptr(stream)
+    vp = values.data_ptr() if N else None
+    lp = list_n.data_ptr() if L else None
+    st = _lib().gc_encode_device_plan(C.byref(prm), vp, lp, L, N, int(delta), *[o.data_ptr() for o in offs],
+                                      ws.data_ptr(), ws.numel(), sizes.ctypes.data, sp)
+    if st:
+        raise GcError(st, "gc_encode_device_plan")
+    ctrl = torch.empty(max(int(sizes[0]), 16), dtype=torch.uint8, device=dev)
+    data = torch.empty(max(int(sizes[1]), 1) * 4, dtype=torch.int32, device=dev)
+    exc = torch.empty(max(int(sizes[2]), 16), dtype=torch.uint8, device=dev)
+    st = _lib().gc_encode_device_write(C.byref(prm), vp, lp, L, N, int(delta), offs[3].data_ptr(),
+                                       sizes.ctypes.data, ctrl.data_ptr(), data.data_ptr(),
+                                       exc.data_ptr(), ws.data_ptr(), ws.numel(), sp)
+    if st:
+        raise GcError(st, "gc_encode_device_write")
+    tensors = dict(list_n=list_n.view(torch.int32), ctrl_off=offs[0], data_off=offs[1],
+                   exc_off=offs[2], out_off=offs[3], ctrl=ctrl[:int(sizes[0])],
+                   data=data[:4 * int(sizes[1])], exc=exc[:int(sizes[2])])
+    return DeviceBatch(codec, variant, frame_quads, L, N, tensors, int(sizes[0]), int(sizes[1]),
+                       int(sizes[2]))
 
 
 def to_device(hb: HostBatch, device="cuda", pin: bool = False) -> DeviceBatch:

@@ -1,0 +1,87 @@
+"""GPU encoder of the frame codecs (-m gpu): Group-PFD (variant 0,
+P:L402-416) and SIMD-BP128 (variant 1) encoded on the device must equal the oracle
+encoder's streams and directory byte for byte, and decode back (through the GPU decoder) to
+the oracle's values.  Bar: bit-exact."""
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1502_01916_b200 import gc  # noqa: E402
+
+KEYS = ("ctrl_off", "data_off", "exc_off", "out_off")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1502_01916_b200 import build
+    build.build()
+    torch.cuda.init()
+
+
+def check(values, list_n, variant, F=32, zeta=(1, 10), delta=False):
+    ref = O.encode_batch(values, list_n, O.GROUP_PFD, variant, delta=delta, frame_quads=F,
+                         zeta=zeta, threads=4)
+    v = torch.from_numpy(np.ascontiguousarray(values, np.uint32).view(np.int32)).cuda()
+    ln = torch.from_numpy(np.ascontiguousarray(list_n, np.uint32).view(np.int32)).cuda()
+    db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, delta=delta, frame_quads=F, zeta=zeta)
+    torch.cuda.synchronize()
+    t = db.tensors
+    for k in KEYS:
+        assert np.array_equal(t[k].cpu().numpy().view(np.uint64), ref[k]), k
+    assert np.array_equal(t["ctrl"].cpu().numpy(), ref["ctrl"])
+    assert np.array_equal(t["data"].cpu().numpy().view(np.uint32).reshape(-1, 4), ref["data"])
+    assert np.array_equal(t["exc"].cpu().numpy(), ref["exc"])
+    out, ws = gc.decode_dgaps(db)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) == 0
+    want = O.decode_batch(ref, dgaps=True, threads=4)
+    assert np.array_equal(out[:db.total_out].cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("variant", [0, 1], ids=["G-PFD", "BP128"])
+@pytest.mark.parametrize("F", [32, 128])
+def test_random_ragged(variant, F):
+    rng = np.random.default_rng(40 + variant + F)
+    for n_lists, max_len, bits, spike in ((1, 5, 3, 0.0), (40, 700, 9, 0.05), (300, 3000, 14, 0.08),
+                                          (20, 40000, 20, 0.01), (50, 300, 32, 0.0)):
+        w = gen.random_lists(rng, n_lists, max_len, bits, spike)
+        check(w.values, w.list_n, variant, F)
+
+
+@pytest.mark.parametrize("zeta", [(1, 10), (3, 10), (1, 50), (0, 1)])
+def test_pfd_zeta(zeta):
+    w = gen.config(3, scale=1 / 512)
+    check(w.values, w.list_n, 0, 32, zeta)
+
+
+def test_delta_docids_and_empty_lists():
+    """docIDs in (config 5's shape: Zipf lengths, 32-bit docIDs), the d-gaps taken on the
+    device; empty lists between non-empty ones."""
+    w = gen.config(5, scale=2 ** -16)
+    ln = w.list_n.copy()
+    ln[::7] = 0
+    vals = np.concatenate([np.sort(np.random.default_rng(3).choice(1 << 30, int(n), replace=False))
+                           .astype(np.uint32) for n in ln]) if ln.sum() else np.zeros(0, np.uint32)
+    for variant in (0, 1):
+        check(vals, ln, variant, 32, delta=True)
+
+
+@pytest.mark.parametrize("variant", [0, 1], ids=["G-PFD", "BP128"])
+def test_config3_full_size(variant):
+    """BASELINE config 3 at full size (2^28 gaps in one list)."""
+    w = gen.config(3)
+    check(w.values, w.list_n, variant, 32)
+
+
+def test_other_codecs_refused():
+    v = torch.zeros(16, dtype=torch.int32, device="cuda")
+    ln = torch.tensor([16], dtype=torch.int32, device="cuda")
+    with pytest.raises(gc.GcError):
+        gc.encode_device(v, ln, gc.GROUP_SCHEME, 0)
