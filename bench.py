@@ -213,30 +213,40 @@ def run_reference(args, rank, world):
 
 
 def run_encode(args, dev):
-    """--encode: the GPU encoder of the frame codecs (Group-PFD, SIMD-BP128; SURVEY §8(f)
-    rank 1) on config 3's gaps resident in HBM: ints/s per codec (gc_encode_device_plan +
-    _write, events on the stream; plan reads the stream sizes back, a host sync), with the
-    oracle encoder on the host cores beside it (bounded sample)."""
+    """--encode: the GPU encoders on the config's gaps resident in HBM:
+    config 2 -> Group-Scheme binary + complete unary (8 variants), config 3 -> Group-PFD and
+    SIMD-BP128.  ints/s per codec (gc_encode_device_plan + _write, events on the stream; plan
+    reads the stream sizes back, a host sync), with the oracle encoder on the host cores
+    beside it (bounded sample)."""
     import torch
     import gen
     import oracle as O
     from paper_1502_01916_b200 import gc
-    w = gen.config(3, scale=args.scale)
+    k = args.config if args.config in (2, 3) else 3
+    w = gen.config(k, scale=args.scale)
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    if k == 2:
+        codecs = [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd)) for cg, kd in gc.GSC_VARIANTS
+                  if kd != "IU"]
+    else:
+        codecs = [(gc.GROUP_PFD, 0), (gc.GROUP_PFD, 1)]
     v = torch.from_numpy(w.values.view(np.int32)).to(dev)
     ln = torch.from_numpy(w.list_n.view(np.int32)).to(dev)
     per, tot_ms, tot_bytes = {}, 0.0, 0
     stream = torch.cuda.current_stream(dev)
-    for variant in (0, 1):
-        label = gc.codec_label(gc.GROUP_PFD, variant)
-        db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+
+    def enc(c, var):
+        return gc.encode_device(v, ln, c, var, frame_quads=32, zeta=zeta)
+    for codec, variant in codecs:
+        label = gc.codec_label(codec, variant)
+        db = enc(codec, variant)
         for _ in range(args.warmup):
-            db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+            db = enc(codec, variant)
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            db = gc.encode_device(v, ln, gc.GROUP_PFD, variant, frame_quads=32, zeta=zeta)
+            db = enc(codec, variant)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms = e0.elapsed_time(e1) / args.steps
@@ -250,16 +260,18 @@ def run_encode(args, dev):
         del db
     peak, peak_src = peaks()
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9
-    # the oracle encoder on a bounded sample of the same gaps
+    # the oracle encoder on a bounded sample of the same gaps (its first lists)
     threads = len(os.sched_getaffinity(0))
-    ns = min(w.n_ints, 1 << 24)
+    cs = np.cumsum(w.list_n.astype(np.int64))
+    nl = max(1, int(np.searchsorted(cs, min(int(cs[-1]), 1 << 24))))
+    ns = int(cs[nl - 1])
     t0 = time.perf_counter()
-    O.encode_batch(w.values[:ns], np.array([ns], np.uint32), O.GROUP_PFD, 0, zeta=zeta,
+    O.encode_batch(w.values[:ns], w.list_n[:nl], codecs[0][0], codecs[0][1], zeta=zeta,
                    threads=threads)
     t_cpu = time.perf_counter() - t0
     line = {
-        "metric": "encoded uint32 ints/sec (GPU frame encoder, Group-PFD + SIMD-BP128)",
-        "value": 2 * w.n_ints / (tot_ms / 1e3), "unit": "ints/s", "n_gpus": 1,
+        "metric": "encoded uint32 ints/sec (GPU encoders)",
+        "value": len(codecs) * w.n_ints / (tot_ms / 1e3), "unit": "ints/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms,
         "higher_is_better": True, "dtype": "u32", "data": "synthetic",
         "config": {"workload": w.name, "n_ints": w.n_ints, "codecs": list(per)},
@@ -269,8 +281,8 @@ def run_encode(args, dev):
         "per_codec": per,
         "cpu_baseline": {"kind": "oracle", "value": ns / t_cpu, "unit": "ints/s",
                          "cores": threads,
-                         "sample": f"first {ns} gaps, Group-PFD, gco_encode_batch (one list, so "
-                                   "one thread does the work)"},
+                         "sample": f"first {nl} lists ({ns} ints), {gc.codec_label(*codecs[0])}, "
+                                   "gco_encode_batch (threads split by list)"},
     }
     print(json.dumps(line), flush=True)
 

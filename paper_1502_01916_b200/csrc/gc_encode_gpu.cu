@@ -322,6 +322,141 @@ __global__ void k_fr_dir(Dir D, uint64_t* ctrl_off, uint64_t* data_off, uint64_t
   exc_off[l] = D.exb_off[f];
 }
 
+// ------------------------------------------------------------------ Group-Scheme (B, CU)
+// Binary and complete-unary LD (A12-A18).  Per quad: u = ceil(width(quad max) /
+// CG) (Eq. 1 with the outer ceiling, A12), BW = CG*u (Eq. 2).  Global exclusive scans over
+// all quads of BW (and, for CU, of the code length u) give every quad's offsets: a list's
+// base is the scan at its first quad and its sizes are differences of the scan, so no
+// segmented scan is needed.  Binary fields sit at closed-form places (A18); unary codes
+// (u-1 ones then a 0, MSB-first in address order, A15/A16) and the data bits (high-first
+// split, A3) are OR-ed into the zeroed streams.
+struct Gsc {
+  const uint32_t* values;
+  const uint32_t* list_n;
+  uint64_t n_lists;
+  int delta;
+  uint32_t cg, kind;       // CG, 0 binary / 1 complete unary
+  uint64_t* out_off;       // [L+1]
+  uint64_t* quad_off;      // [L+1] first quad of each list
+  uint64_t n_quads;
+  uint8_t* u;              // [n_quads] units per quad
+  uint64_t* bw_off;        // [n_quads+1] exclusive scan of BW (lane bits)
+  uint64_t* cu_off;        // [n_quads+1] exclusive scan of u (CU control bits)
+};
+struct GetQuads {
+  const uint32_t* list_n;
+  __device__ uint64_t operator()(uint64_t i) const { return (list_n[i] + 3ull) >> 2; }
+};
+struct GetBW {
+  const uint8_t* u;
+  uint32_t cg;
+  __device__ uint64_t operator()(uint64_t i) const { return (uint64_t)cg * u[i]; }
+};
+struct GetU {
+  const uint8_t* u;
+  __device__ uint64_t operator()(uint64_t i) const { return u[i]; }
+};
+__device__ __forceinline__ uint64_t list_of_quad(const Gsc& G, uint64_t g) {
+  uint64_t a = 0, b = G.n_lists;  // the last list whose first quad is <= g
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (G.quad_off[m] <= g) a = m;
+    else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ void gsc_quad(const Gsc& G, uint64_t l, uint64_t j, uint32_t* v) {
+  const uint32_t n = G.list_n[l];
+  const uint64_t e = G.out_off[l] + 4 * j;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const uint64_t p = 4 * j + t;
+    uint32_t x = 0;
+    if (p < n) {
+      x = G.values[e + t];
+      if (G.delta && p > 0) x -= G.values[e + t - 1];  // d-gaps
+    }
+    v[t] = x;
+  }
+}
+__global__ void k_gsc_units(Gsc G) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_quads) return;
+  const uint64_t l = list_of_quad(G, g);
+  uint32_t v[4];
+  gsc_quad(G, l, g - G.quad_off[l], v);
+  const uint32_t w = width_of(v[0] | v[1] | v[2] | v[3]);  // width of the quad max (A9)
+  G.u[g] = (uint8_t)((w + G.cg - 1) / G.cg);               // A12
+}
+// per list: control bytes (4-byte padded) and data vectors
+__global__ void k_gsc_sizes(Gsc G, uint64_t* cb, uint64_t* vecs) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= G.n_lists) return;
+  const uint64_t qs = G.quad_off[l], qe = G.quad_off[l + 1], Q = qe - qs;
+  uint64_t bytes;
+  if (G.kind == 1) {
+    bytes = (G.cu_off[qe] - G.cu_off[qs] + 7) / 8;
+  } else {  // A18: CG 1 three 5-bit fields per 16-bit unit, CG 2/4 two per byte, CG 8 four
+    bytes = G.cg == 1 ? 2 * ((Q + 2) / 3) : (G.cg == 8 ? (Q + 3) / 4 : (Q + 1) / 2);
+  }
+  cb[l] = 4 * ((bytes + 3) / 4);
+  vecs[l] = (G.bw_off[qe] - G.bw_off[qs] + 31) / 32;
+}
+__device__ __forceinline__ void or_byte_bits(uint8_t* base, uint64_t byte, uint32_t bits) {
+  // OR `bits` (8 bits) into the byte at `byte` through its aligned 32-bit word
+  if (!bits) return;
+  uint32_t* w = reinterpret_cast<uint32_t*>(base + (byte & ~3ull));
+  atomicOr(w, bits << (8 * (uint32_t)(byte & 3)));
+}
+__global__ void k_gsc_write(Gsc G, const uint64_t* ctrl_off, const uint64_t* data_off, uint8_t* ctrl,
+                            uint32_t* data) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_quads) return;
+  const uint64_t l = list_of_quad(G, g), qs = G.quad_off[l], j = g - qs;
+  const uint32_t u = G.u[g], bw = G.cg * u;
+  // control
+  const uint64_t cbase = ctrl_off[l];
+  if (G.kind == 1) {  // (u-1) ones then a 0, MSB-first in address order
+    const uint64_t c = G.cu_off[g] - G.cu_off[qs];
+    for (uint64_t i = c; i + 1 < c + u;) {  // the ones, a byte at a time
+      const uint64_t byte = i >> 3;
+      const uint64_t e = c + u - 1 - 8 * byte;
+      const uint32_t b0 = (uint32_t)(i & 7), b1 = e < 8 ? (uint32_t)e : 8u;
+      const uint32_t bits = ((0xFFu >> b0) & ~(0xFFu >> b1)) & 0xFFu;  // bits b0..b1-1 from the MSB
+      or_byte_bits(ctrl, cbase + byte, bits);
+      i = 8 * byte + b1;
+    }
+  } else {
+    const uint32_t f = u - 1;  // A13: binary stores u - 1
+    uint64_t byte;
+    uint32_t sh;
+    if (G.cg == 1) { byte = 2 * (j / 3); sh = 5 * (uint32_t)(j % 3); }
+    else if (G.cg == 2) { byte = j / 2; sh = 4 * (uint32_t)(j % 2); }
+    else if (G.cg == 4) { byte = j / 2; sh = 3 * (uint32_t)(j % 2); }
+    else { byte = j / 4; sh = 2 * (uint32_t)(j % 4); }
+    const uint64_t a = cbase + byte;  // (a 16-bit unit never crosses its aligned word)
+    atomicOr(reinterpret_cast<uint32_t*>(ctrl + (a & ~3ull)), f << (sh + 8 * (uint32_t)(a & 3)));
+  }
+  // data: the 4 lane values at the quad's lane-bit position (A3 split)
+  uint32_t v[4];
+  gsc_quad(G, l, j, v);
+  const uint64_t pos = data_off[l] * 32 + (G.bw_off[g] - G.bw_off[qs]);
+  const uint64_t m = pos >> 5;
+  const uint32_t off = (uint32_t)(pos & 31), rem = 32u - off;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const uint32_t x = low_bits(v[t], bw);
+    if (!x) continue;
+    if (bw <= rem) {
+      atomicOr(&data[4 * m + t], x << off);
+    } else {
+      const uint32_t lo = bw - rem;
+      atomicOr(&data[4 * m + t], (x >> lo) << off);
+      atomicOr(&data[4 * (m + 1) + t], low_bits(x, lo));
+    }
+  }
+}
+
 struct WsLayout {
   uint64_t frame_off, rec, vec_off, exb_off, sums, bytes;
 };
@@ -340,14 +475,69 @@ inline WsLayout ws_layout(uint64_t n_lists, uint64_t total, uint32_t F) {
   return L;
 }
 
+struct GscWs {
+  uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, sums, bytes;
+};
+inline GscWs gsc_ws_layout(uint64_t n_lists, uint64_t total) {
+  auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
+  const uint64_t nq = total / 4 + n_lists + 1;  // >= sum over lists of ceil(n/4)
+  const uint64_t nsum = (std::max(nq, n_lists) + 1) / kScanB + 2;
+  GscWs L;
+  L.quad_off = 0;
+  L.u = L.quad_off + al(8 * (n_lists + 1));
+  L.bw_off = L.u + al(nq);
+  L.cu_off = L.bw_off + al(8 * (nq + 1));
+  L.c_off = L.cu_off + al(8 * (nq + 1));
+  L.d_off = L.c_off + al(8 * (n_lists + 1));
+  L.sums = L.d_off + al(8 * (n_lists + 1));
+  L.bytes = L.sums + al(8 * (nsum + 1));
+  return L;
+}
+struct GetArr {
+  const uint64_t* p;
+  __device__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+__global__ void k_copy_u64(const uint64_t* a, uint64_t* b, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
 }  // namespace gce
 
 using namespace gce;
 
 namespace {
-bool valid_gpu_params(const gc_encode_params* p) {
-  return p && p->codec == GC_GROUP_PFD && (p->pfd_frame_quads == 32 || p->pfd_frame_quads == 128) &&
+bool is_pfd(const gc_encode_params* p) {
+  return p->codec == GC_GROUP_PFD && (p->pfd_frame_quads == 32 || p->pfd_frame_quads == 128) &&
          p->variant <= 1 && (p->variant == 1 || p->zeta_den > 0);
+}
+bool is_gsc(const gc_encode_params* p) {  // binary or complete unary (IU: host encoder)
+  const uint32_t kind = (p->variant >> 2) & 3u;
+  return p->codec == GC_GROUP_SCHEME && p->variant <= 15 && kind <= 1;
+}
+gc_status refuse(const gc_encode_params* p) {
+  if (!p) return GC_ERR_INVALID_ARGUMENT;
+  if (p->codec != GC_GROUP_PFD && p->codec != GC_GROUP_SCHEME) return GC_ERR_UNKNOWN_CODEC;
+  return GC_ERR_BAD_VARIANT;
+}
+Gsc make_gsc(const gc_encode_params* p, const uint32_t* values, const uint32_t* list_n,
+             uint64_t n_lists, int delta, uint64_t* out_off, void* ws, uint64_t total) {
+  const GscWs L = gsc_ws_layout(n_lists, total);
+  uint8_t* w = (uint8_t*)ws;
+  Gsc G;
+  G.values = values;
+  G.list_n = list_n;
+  G.n_lists = n_lists;
+  G.delta = delta;
+  G.cg = 1u << (p->variant & 3u);
+  G.kind = (p->variant >> 2) & 3u;
+  G.out_off = out_off;
+  G.quad_off = (uint64_t*)(w + L.quad_off);
+  G.n_quads = 0;
+  G.u = w + L.u;
+  G.bw_off = (uint64_t*)(w + L.bw_off);
+  G.cu_off = (uint64_t*)(w + L.cu_off);
+  return G;
 }
 Dir make_dir(const gc_encode_params* p, const uint32_t* values, const uint32_t* list_n,
              uint64_t n_lists, int delta, uint64_t* out_off, void* ws, uint64_t total) {
@@ -376,9 +566,54 @@ extern "C" {
 
 gc_status gc_encode_device_ws_size(const gc_encode_params* p, uint64_t n_lists, uint64_t total_ints,
                                    uint64_t* bytes) {
-  if (!valid_gpu_params(p) || !bytes) return p && p->codec != GC_GROUP_PFD ? GC_ERR_UNKNOWN_CODEC
-                                                                           : GC_ERR_INVALID_ARGUMENT;
-  *bytes = ws_layout(n_lists, total_ints, p->pfd_frame_quads).bytes;
+  if (!p || !bytes) return GC_ERR_INVALID_ARGUMENT;
+  if (is_pfd(p)) *bytes = ws_layout(n_lists, total_ints, p->pfd_frame_quads).bytes;
+  else if (is_gsc(p)) *bytes = gsc_ws_layout(n_lists, total_ints).bytes;
+  else return refuse(p);
+  return GC_OK;
+}
+
+static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, const uint32_t* list_n,
+                          uint64_t n_lists, uint64_t total_ints, int delta, uint64_t* ctrl_off,
+                          uint64_t* data_off, uint64_t* exc_off, uint64_t* out_off, void* ws,
+                          uint64_t* sizes, cudaStream_t st) {
+  const GscWs L = gsc_ws_layout(n_lists, total_ints);
+  Gsc G = make_gsc(p, values, list_n, n_lists, delta, out_off, ws, total_ints);
+  uint8_t* w = (uint8_t*)ws;
+  uint64_t* sums = (uint64_t*)(w + L.sums);
+  uint64_t* c_off = (uint64_t*)(w + L.c_off);
+  uint64_t* d_off = (uint64_t*)(w + L.d_off);
+  if (scan_u64(GetListN{list_n}, n_lists, out_off, sums, st) != cudaSuccess ||
+      scan_u64(GetQuads{list_n}, n_lists, G.quad_off, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  uint64_t nq = 0, tot = 0;
+  if (cudaMemcpyAsync(&nq, G.quad_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&tot, out_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  if (tot != total_ints) return GC_ERR_INVALID_ARGUMENT;
+  G.n_quads = nq;
+  if (nq) k_gsc_units<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(G);
+  if (scan_u64(GetBW{G.u, G.cg}, nq, G.bw_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (G.kind == 1 && scan_u64(GetU{G.u}, nq, G.cu_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (n_lists) k_gsc_sizes<<<(unsigned)((n_lists + 255) / 256), 256, 0, st>>>(G, c_off, d_off);
+  // exclusive scans in place: the per-list sizes become the list offsets
+  if (scan_u64(GetArr{c_off}, n_lists, c_off, sums, st) != cudaSuccess ||
+      scan_u64(GetArr{d_off}, n_lists, d_off, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  const unsigned nb = (unsigned)((n_lists + 1 + 255) / 256);
+  k_copy_u64<<<nb, 256, 0, st>>>(c_off, ctrl_off, n_lists + 1);
+  k_copy_u64<<<nb, 256, 0, st>>>(d_off, data_off, n_lists + 1);
+  if (cudaMemsetAsync(exc_off, 0, 8 * (n_lists + 1), st) != cudaSuccess) return GC_ERR_CUDA;
+  uint64_t ct = 0, vt = 0;
+  if (cudaMemcpyAsync(&ct, c_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&vt, d_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  sizes[0] = 16 * ((ct + 15) / 16);
+  sizes[1] = vt;
+  sizes[2] = 0;
+  sizes[3] = nq;
   return GC_OK;
 }
 
@@ -387,13 +622,18 @@ gc_status gc_encode_device_plan(const gc_encode_params* p, const uint32_t* value
                                 int delta, uint64_t* ctrl_off, uint64_t* data_off,
                                 uint64_t* exc_off, uint64_t* out_off, void* ws, uint64_t ws_bytes,
                                 uint64_t* sizes, void* stream) {
-  if (!valid_gpu_params(p)) return p && p->codec != GC_GROUP_PFD ? GC_ERR_UNKNOWN_CODEC : GC_ERR_BAD_VARIANT;
+  uint64_t need = 0;
+  const gc_status s0 = gc_encode_device_ws_size(p, n_lists, total_ints, &need);
+  if (s0 != GC_OK) return s0;
   if (!ws || !sizes || !ctrl_off || !data_off || !exc_off || !out_off ||
       (n_lists && !list_n) || (total_ints && !values))
     return GC_ERR_INVALID_ARGUMENT;
-  const WsLayout L = ws_layout(n_lists, total_ints, p->pfd_frame_quads);
-  if (ws_bytes < L.bytes) return GC_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < need) return GC_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = (cudaStream_t)stream;
+  if (is_gsc(p))
+    return gsc_plan(p, values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
+                    out_off, ws, sizes, st);
+  const WsLayout L = ws_layout(n_lists, total_ints, p->pfd_frame_quads);
   Dir D = make_dir(p, values, list_n, n_lists, delta, out_off, ws, total_ints);
   uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
   // list offsets and first frames
@@ -432,19 +672,31 @@ gc_status gc_encode_device_write(const gc_encode_params* p, const uint32_t* valu
                                  int delta, const uint64_t* out_off, const uint64_t* sizes,
                                  uint8_t* ctrl, void* data, uint8_t* exc, void* ws,
                                  uint64_t ws_bytes, void* stream) {
-  if (!valid_gpu_params(p)) return p && p->codec != GC_GROUP_PFD ? GC_ERR_UNKNOWN_CODEC : GC_ERR_BAD_VARIANT;
-  const WsLayout L = ws_layout(n_lists, total_ints, p->pfd_frame_quads);
-  if (!ws || ws_bytes < L.bytes) return GC_ERR_WORKSPACE_TOO_SMALL;
+  uint64_t need = 0;
+  const gc_status s0 = gc_encode_device_ws_size(p, n_lists, total_ints, &need);
+  if (s0 != GC_OK) return s0;
+  if (!ws || ws_bytes < need) return GC_ERR_WORKSPACE_TOO_SMALL;
   if (!sizes || (sizes[0] && !ctrl) || (sizes[1] && !data) || (sizes[2] && !exc) ||
       ((uintptr_t)data & 15) || ((uintptr_t)ctrl & 3))
     return GC_ERR_INVALID_ARGUMENT;
   cudaStream_t st = (cudaStream_t)stream;
-  Dir D = make_dir(p, values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);
-  D.n_frames = sizes[3];
-  // padding bytes of the control / exception streams are zero
+  // padding bytes of the control / exception streams are zero; the OR-packed ones start at 0
   if ((sizes[0] && cudaMemsetAsync(ctrl, 0, sizes[0], st) != cudaSuccess) ||
       (sizes[2] && cudaMemsetAsync(exc, 0, sizes[2], st) != cudaSuccess))
     return GC_ERR_CUDA;
+  if (is_gsc(p)) {
+    const GscWs L = gsc_ws_layout(n_lists, total_ints);
+    Gsc G = make_gsc(p, values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);
+    G.n_quads = sizes[3];
+    if (sizes[1] && cudaMemsetAsync(data, 0, 16 * sizes[1], st) != cudaSuccess) return GC_ERR_CUDA;
+    if (G.n_quads)
+      k_gsc_write<<<(unsigned)((G.n_quads + 255) / 256), 256, 0, st>>>(
+          G, (const uint64_t*)((uint8_t*)ws + L.c_off), (const uint64_t*)((uint8_t*)ws + L.d_off),
+          ctrl, (uint32_t*)data);
+    return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  }
+  Dir D = make_dir(p, values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);
+  D.n_frames = sizes[3];
   if (D.n_frames) {
     const uint64_t blocks = (D.n_frames + kWarpsPerBlock - 1) / kWarpsPerBlock;
     k_fr_write<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(D, ctrl, (uint4*)data, exc);

@@ -80,8 +80,55 @@ def test_config3_full_size(variant):
     check(w.values, w.list_n, variant, 32)
 
 
+GSC_BCU = [(cg, k) for cg in (1, 2, 4, 8) for k in ("B", "CU")]
+
+
+def check_gsc(values, list_n, variant, delta=False):
+    ref = O.encode_batch(values, list_n, O.GROUP_SCHEME, variant, delta=delta, threads=4)
+    v = torch.from_numpy(np.ascontiguousarray(values, np.uint32).view(np.int32)).cuda()
+    ln = torch.from_numpy(np.ascontiguousarray(list_n, np.uint32).view(np.int32)).cuda()
+    db = gc.encode_device(v, ln, gc.GROUP_SCHEME, variant, delta=delta)
+    torch.cuda.synchronize()
+    t = db.tensors
+    for k in KEYS:
+        assert np.array_equal(t[k].cpu().numpy().view(np.uint64), ref[k]), k
+    assert np.array_equal(t["ctrl"].cpu().numpy(), ref["ctrl"])
+    assert np.array_equal(t["data"].cpu().numpy().view(np.uint32).reshape(-1, 4), ref["data"])
+    assert db.exc_bytes == len(ref["exc"]) == 0
+    out, ws = gc.decode_dgaps(db)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) == 0
+    assert np.array_equal(out[:db.total_out].cpu().numpy().view(np.uint32),
+                          O.decode_batch(ref, dgaps=True, threads=4))
+
+
+@pytest.mark.parametrize("cg,kind", GSC_BCU, ids=[f"GSC-{c}-{k}" for c, k in GSC_BCU])
+def test_group_scheme_random(cg, kind):
+    """Group-Scheme binary / complete unary encoded on the device."""
+    rng = np.random.default_rng(70 + cg + (kind == "CU"))
+    variant = O.gsc_variant(cg, kind)
+    for n_lists, max_len, bits, spike in ((1, 6, 3, 0.0), (60, 900, 11, 0.05),
+                                          (300, 3000, 20, 0.01), (40, 200, 32, 0.0)):
+        w = gen.random_lists(rng, n_lists, max_len, bits, spike)
+        check_gsc(w.values, w.list_n, variant)
+
+
+def test_group_scheme_config2_full_size():
+    """BASELINE config 2 at full size (2^26 gaps in 10^5 lists), every B / CU variant."""
+    w = gen.config(2)
+    for cg, kind in GSC_BCU:
+        check_gsc(w.values, w.list_n, O.gsc_variant(cg, kind))
+
+
+def test_group_scheme_docids():
+    w = gen.config(1)  # docIDs: the d-gaps are taken on the device
+    check_gsc(w.values, w.list_n, O.gsc_variant(4, "CU"), delta=True)
+
+
 def test_other_codecs_refused():
     v = torch.zeros(16, dtype=torch.int32, device="cuda")
     ln = torch.tensor([16], dtype=torch.int32, device="cuda")
-    with pytest.raises(gc.GcError):
-        gc.encode_device(v, ln, gc.GROUP_SCHEME, 0)
+    for codec, variant in ((gc.GROUP_SCHEME, O.gsc_variant(8, "IU")), (gc.GROUP_AFOR, 0),
+                           (gc.GROUP_SIMPLE, 0)):
+        with pytest.raises(gc.GcError):
+            gc.encode_device(v, ln, codec, variant)
