@@ -213,30 +213,32 @@ def run_reference(args, rank, world):
 
 
 def run_encode(args, dev):
-    """--encode: the GPU encoders on the config's gaps resident in HBM:
-    config 2 -> Group-Scheme binary + complete unary (8 variants), config 3 -> Group-PFD and
-    SIMD-BP128.  ints/s per codec (gc_encode_device_plan + _write, events on the stream; plan
+    """--encode: the GPU encoders on the config's inputs resident in HBM:
+    config 1 -> Group-Simple (docIDs in), config 2 -> Group-Scheme binary + complete unary
+    (8 variants), config 3 -> Group-PFD and SIMD-BP128, config 4 -> Group-AFOR.  ints/s per codec (gc_encode_device_plan + _write, events on the stream; plan
     reads the stream sizes back, a host sync), with the oracle encoder on the host cores
     beside it (bounded sample)."""
     import torch
     import gen
     import oracle as O
     from paper_1502_01916_b200 import gc
-    k = args.config if args.config in (2, 3) else 3
+    k = args.config if args.config in (1, 2, 3, 4) else 3
     w = gen.config(k, scale=args.scale)
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
     if k == 2:
         codecs = [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd)) for cg, kd in gc.GSC_VARIANTS
                   if kd != "IU"]
-    else:
+    elif k == 3:
         codecs = [(gc.GROUP_PFD, 0), (gc.GROUP_PFD, 1)]
+    else:
+        codecs = [(gc.GROUP_SIMPLE if k == 1 else gc.GROUP_AFOR, 0)]
     v = torch.from_numpy(w.values.view(np.int32)).to(dev)
     ln = torch.from_numpy(w.list_n.view(np.int32)).to(dev)
     per, tot_ms, tot_bytes = {}, 0.0, 0
     stream = torch.cuda.current_stream(dev)
 
     def enc(c, var):
-        return gc.encode_device(v, ln, c, var, frame_quads=32, zeta=zeta)
+        return gc.encode_device(v, ln, c, var, delta=w.delta, frame_quads=32, zeta=zeta)
     for codec, variant in codecs:
         label = gc.codec_label(codec, variant)
         db = enc(codec, variant)
@@ -266,8 +268,8 @@ def run_encode(args, dev):
     nl = max(1, int(np.searchsorted(cs, min(int(cs[-1]), 1 << 24))))
     ns = int(cs[nl - 1])
     t0 = time.perf_counter()
-    O.encode_batch(w.values[:ns], w.list_n[:nl], codecs[0][0], codecs[0][1], zeta=zeta,
-                   threads=threads)
+    O.encode_batch(w.values[:ns], w.list_n[:nl], codecs[0][0], codecs[0][1], delta=w.delta,
+                   zeta=zeta, threads=threads)
     t_cpu = time.perf_counter() - t0
     line = {
         "metric": "encoded uint32 ints/sec (GPU encoders)",

@@ -475,6 +475,292 @@ inline WsLayout ws_layout(uint64_t n_lists, uint64_t total, uint32_t F) {
   return L;
 }
 
+// ------------------------------------------------------------------ Group-AFOR
+// P:L392 §6.1 with the readings A22-A25: the quad-max widths of a list padded with zero
+// quads (width 1) to a multiple of 8; a backward DP over the 8-quad slots, frame lengths
+// L tried in the order 32, 16, 8 and replaced only on strict improvement of
+// 8 + 128*ceil(L*bw/32) + (cost of the rest); header byte = code(8/16/32 -> 0/1/2) |
+// (bw-1) << 2; each frame's data starts a fresh vector.  Lists in parallel (one thread
+// runs a list's DP over precomputed 8-quad block maxima), frames written by one warp each.
+struct Afor {
+  const uint32_t* values;
+  const uint32_t* list_n;
+  uint64_t n_lists;
+  int delta;
+  uint64_t* out_off;     // [L+1]
+  uint64_t* blk_off;     // [L+1] first 8-quad block of each list
+  uint64_t n_blocks;
+  uint8_t* bmax;         // [n_blocks] max quad width of the block
+  uint8_t* fstart;       // [n_blocks] L of the frame starting here, 0 if none
+  uint8_t* fbw;          // [n_blocks] its bw
+  uint32_t* fvec;        // [n_blocks] its first vector within the list
+  uint32_t* fidx;        // [n_blocks] its index within the list
+  uint64_t* cost;        // [n_blocks] DP cost of the list from this block on
+  uint64_t* nf;          // [n_lists] frames of each list
+  uint64_t* nv;          // [n_lists] vectors of each list
+};
+struct GetBlocks {
+  const uint32_t* list_n;
+  __device__ uint64_t operator()(uint64_t i) const {
+    const uint64_t Q = (list_n[i] + 3ull) >> 2;
+    return (Q + 7) / 8;
+  }
+};
+__device__ __forceinline__ uint64_t list_of_block(const Afor& A, uint64_t g) {
+  uint64_t a = 0, b = A.n_lists;
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (A.blk_off[m] <= g) a = m;
+    else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ void afor_quad(const Afor& A, uint64_t l, uint64_t j, uint32_t* v) {
+  const uint32_t n = A.list_n[l];
+  const uint64_t e = A.out_off[l] + 4 * j;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const uint64_t p = 4 * j + t;
+    uint32_t x = 0;
+    if (p < n) {
+      x = A.values[e + t];
+      if (A.delta && p > 0) x -= A.values[e + t - 1];  // d-gaps
+    }
+    v[t] = x;
+  }
+}
+__global__ void k_afor_bmax(Afor A) {  // one thread per 8-quad block
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= A.n_blocks) return;
+  const uint64_t l = list_of_block(A, g), s = g - A.blk_off[l];
+  uint32_t m = 1;
+  for (uint32_t t = 0; t < 8; t++) {
+    uint32_t v[4];
+    afor_quad(A, l, 8 * s + t, v);  // (zero past the list: width 1, A25)
+    m = max(m, width_of(v[0] | v[1] | v[2] | v[3]));
+  }
+  A.bmax[g] = (uint8_t)m;
+}
+__global__ void k_afor_dp(Afor A) {  // one thread per list
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= A.n_lists) return;
+  const uint64_t b0 = A.blk_off[l], S = A.blk_off[l + 1] - b0;
+  for (int64_t s = (int64_t)S - 1; s >= 0; s--) {
+    uint64_t best = ~0ull;
+    uint8_t bl = 8;
+    uint32_t bw = 1;
+    for (uint32_t L = 8; L <= 32; L <<= 1) {  // bw of the first L quads from s
+      if ((uint64_t)s + L / 8 > S) break;
+      for (uint32_t k = (L == 8 ? 0 : L / 16); k < L / 8; k++) bw = max(bw, (uint32_t)A.bmax[b0 + s + k]);
+      // candidates in the oracle's order 32, 16, 8: evaluate all, pick by that order below
+      const uint64_t rest = (uint64_t)s + L / 8 < S ? A.cost[b0 + s + L / 8] : 0ull;
+      const uint64_t c = 8 + 128 * (((uint64_t)L * bw + 31) / 32) + rest;
+      // strict improvement in the order 32, 16, 8 == the smallest cost, ties to the longest L
+      if (c < best || (c == best && L > bl)) {
+        best = c;
+        bl = (uint8_t)L;
+      }
+    }
+    A.cost[b0 + s] = best;
+    A.fstart[b0 + s] = bl;  // (the choice; turned into frame starts below)
+  }
+  // forward: the frames, their bw, vector offsets and indices
+  uint64_t f = 0, vec = 0;
+  uint64_t s = 0;
+  while (s < S) {
+    const uint32_t L = A.fstart[b0 + s];
+    uint32_t bw = 1;
+    for (uint32_t k = 0; k < L / 8; k++) bw = max(bw, (uint32_t)A.bmax[b0 + s + k]);
+    for (uint32_t k = 1; k < L / 8; k++) A.fstart[b0 + s + k] = 0;
+    A.fbw[b0 + s] = (uint8_t)bw;
+    A.fvec[b0 + s] = (uint32_t)vec;
+    A.fidx[b0 + s] = (uint32_t)f;
+    vec += ((uint64_t)L * bw + 31) / 32;
+    f++;
+    s += L / 8;
+  }
+  A.nf[l] = 4 * ((f + 3) / 4);  // control bytes: one header per frame, padded to 4
+  A.nv[l] = vec;
+}
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_afor_write(Afor A, const uint64_t* ctrl_off,
+                                                                   const uint64_t* data_off,
+                                                                   uint8_t* ctrl, uint4* data) {
+  __shared__ uint32_t s_pack[kWarpsPerBlock][4 * 32 + 4];
+  const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint64_t g = (uint64_t)blockIdx.x * kWarpsPerBlock + wi;
+  if (g >= A.n_blocks) return;
+  const uint32_t L = A.fstart[g];
+  if (!L) return;  // (warp-uniform)
+  const uint64_t l = list_of_block(A, g), s = g - A.blk_off[l];
+  const uint32_t bw = A.fbw[g];
+  if (lane == 0) {
+    const uint32_t code = L == 8 ? 0u : (L == 16 ? 1u : 2u);
+    ctrl[ctrl_off[l] + A.fidx[g]] = (uint8_t)(code | ((bw - 1) << 2));  // A22 header byte
+  }
+  uint32_t* pk = s_pack[wi];
+  for (uint32_t w = lane; w < 4 * 32 + 4; w += 32) pk[w] = 0;
+  __syncwarp();
+  if (lane < L) {
+    uint32_t v[4];
+    afor_quad(A, l, 8 * s + lane, v);
+    const uint32_t pos = lane * bw, m = pos >> 5, off = pos & 31u, rem = 32u - off;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const uint32_t x = low_bits(v[t], bw);
+      if (bw <= rem) {
+        atomicOr(&pk[4 * m + t], x << off);
+      } else {
+        const uint32_t lo = bw - rem;
+        atomicOr(&pk[4 * m + t], (x >> lo) << off);
+        atomicOr(&pk[4 * (m + 1) + t], low_bits(x, lo));
+      }
+    }
+  }
+  __syncwarp();
+  const uint32_t nvec = (L * bw + 31) / 32;
+  const uint64_t vb = data_off[l] + A.fvec[g];
+  for (uint32_t m2 = lane; m2 < nvec; m2 += 32)
+    data[vb + m2] = make_uint4(pk[4 * m2], pk[4 * m2 + 1], pk[4 * m2 + 2], pk[4 * m2 + 3]);
+}
+struct AforWs {
+  uint64_t blk_off, bmax, fstart, fbw, fvec, fidx, cost, nf, nv, sums, bytes;
+};
+inline AforWs afor_ws_layout(uint64_t n_lists, uint64_t total) {
+  auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
+  const uint64_t nb = total / 32 + n_lists + 1;  // >= sum over lists of ceil(ceil(n/4)/8)
+  const uint64_t nsum = (std::max(nb, n_lists) + 1) / kScanB + 2;
+  AforWs L;
+  L.blk_off = 0;
+  L.bmax = L.blk_off + al(8 * (n_lists + 1));
+  L.fstart = L.bmax + al(nb);
+  L.fbw = L.fstart + al(nb);
+  L.fvec = L.fbw + al(nb);
+  L.fidx = L.fvec + al(4 * nb);
+  L.cost = L.fidx + al(4 * nb);
+  L.nf = L.cost + al(8 * nb);
+  L.nv = L.nf + al(8 * (n_lists + 1));
+  L.sums = L.nv + al(8 * (n_lists + 1));
+  L.bytes = L.sums + al(8 * (nsum + 1));
+  return L;
+}
+
+// ------------------------------------------------------------------ Group-Simple
+// Algorithm 1 is a greedy over a list's quad maxima.  Its step from any quad
+// depends only on the quad maxima ahead, so every quad's step (selector, quads covered) is
+// computed in parallel; one thread per list then follows the chain from quad 0 (one load
+// per selector) and numbers the selectors; every selector start writes its nibble (low
+// first, A6) and its 128-bit vector (int t of a component at [t*BW, (t+1)*BW), A7).
+__constant__ uint32_t kGsNum[10] = {32, 16, 10, 8, 6, 5, 4, 3, 2, 1};
+__constant__ uint32_t kGsBw[10] = {1, 2, 3, 4, 5, 6, 8, 10, 16, 32};
+struct GsEnc {
+  const uint32_t* values;
+  const uint32_t* list_n;
+  uint64_t n_lists;
+  int delta;
+  uint64_t* out_off;
+  uint64_t* cb;        // [L+1] control bytes (4-padded), then the exclusive scan
+  uint64_t* nv;        // [L+1] selectors = vectors, then the exclusive scan
+  uint64_t* quad_off;  // [L+1] first quad of each list
+  uint32_t* M;         // [quads] quad maxima, precomputed in parallel
+  uint64_t n_quads;
+};
+__device__ __forceinline__ void gs_quad(const GsEnc& E, uint64_t e0, uint32_t n, uint64_t j,
+                                        uint32_t* v) {
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const uint64_t p = 4 * j + t;
+    uint32_t x = 0;
+    if (p < n) {
+      x = E.values[e0 + p];
+      if (E.delta && p > 0) x -= E.values[e0 + p - 1];  // d-gaps
+    }
+    v[t] = x;
+  }
+}
+__global__ void k_gs_qmax(GsEnc E) {  // one thread per quad
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= E.n_quads) return;
+  uint64_t a = 0, b = E.n_lists;  // the last list whose first quad is <= g
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (E.quad_off[m] <= g) a = m;
+    else b = m;
+  }
+  uint32_t v[4];
+  gs_quad(E, E.out_off[a], E.list_n[a], g - E.quad_off[a], v);
+  E.M[g] = max(max(v[0], v[1]), max(v[2], v[3]));
+}
+// one selector of Algorithm 1 at quad j with l quads left: (SEL i, quads covered)
+__device__ __forceinline__ void gs_next(const uint32_t* M, uint64_t j, uint64_t l, uint32_t& sel,
+                                        uint64_t& pos) {
+  uint32_t i;
+  for (i = 0; i <= 9; i++) {
+    const uint64_t nn = kGsNum[i], mask = (1ull << kGsBw[i]) - 1;  // 64-bit mask (A8)
+    const uint64_t lim = nn < l ? nn : l;
+    pos = 0;
+    while (pos < lim && (uint64_t)M[j + pos] <= mask) pos++;
+    if (pos == nn || pos == l) break;
+  }
+  sel = i;
+}
+// the selector Algorithm 1 would emit if one started at quad g, and the quads it covers
+// (every quad in parallel; only the chain from each list's quad 0 is used)
+__global__ void k_gs_step(GsEnc E, uint8_t* sel, uint8_t* cov) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= E.n_quads) return;
+  uint64_t a = 0, b = E.n_lists;
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (E.quad_off[m] <= g) a = m;
+    else b = m;
+  }
+  const uint64_t q0 = E.quad_off[a], j = g - q0, Q = E.quad_off[a + 1] - q0;
+  uint32_t s;
+  uint64_t pos;
+  gs_next(E.M + q0, j, Q - j, s, pos);
+  sel[g] = (uint8_t)s;
+  cov[g] = (uint8_t)pos;
+}
+// per list: follow the chain from quad 0 (one load per selector), number the selectors
+__global__ void k_gs_chase(GsEnc E, const uint8_t* cov, uint32_t* idx) {
+  const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= E.n_lists) return;
+  const uint64_t q0 = E.quad_off[li], Q = E.quad_off[li + 1] - q0;
+  uint64_t j = 0, T = 0;
+  while (j < Q) {
+    idx[q0 + j] = (uint32_t)T++;
+    j += cov[q0 + j];
+  }
+  E.cb[li] = 4 * (((T + 1) / 2 + 3) / 4);  // nibbles, low first (A6), padded to 4 bytes
+  E.nv[li] = T;                            // one vector per selector
+}
+// every selector start: its nibble and its vector (int t of a component at t*BW, A7)
+__global__ void k_gs_write(GsEnc E, const uint8_t* sel, const uint8_t* cov, const uint32_t* idx,
+                           uint8_t* ctrl, uint4* data) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= E.n_quads || idx[g] == ~0u) return;
+  uint64_t a = 0, b = E.n_lists;
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (E.quad_off[m] <= g) a = m;
+    else b = m;
+  }
+  const uint32_t s = idx[g], SEL = sel[g], c = cov[g], BW = kGsBw[SEL];
+  const uint64_t q0 = E.quad_off[a], e0 = E.out_off[a];
+  const uint32_t n = E.list_n[a];
+  uint32_t cmp[4] = {0, 0, 0, 0};
+  for (uint32_t t = 0; t < c; t++) {
+    uint32_t v[4];
+    gs_quad(E, e0, n, g - q0 + t, v);
+#pragma unroll
+    for (int k = 0; k < 4; k++) cmp[k] |= v[k] << (t * BW);
+  }
+  data[E.nv[a] + s] = make_uint4(cmp[0], cmp[1], cmp[2], cmp[3]);
+  const uint64_t byte = E.cb[a] + (s >> 1);
+  atomicOr(reinterpret_cast<uint32_t*>(ctrl + (byte & ~3ull)),
+           (SEL << (4 * (s & 1))) << (8 * (uint32_t)(byte & 3)));
+}
+
 struct GscWs {
   uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, sums, bytes;
 };
@@ -515,10 +801,68 @@ bool is_gsc(const gc_encode_params* p) {  // binary or complete unary (IU: host 
   const uint32_t kind = (p->variant >> 2) & 3u;
   return p->codec == GC_GROUP_SCHEME && p->variant <= 15 && kind <= 1;
 }
+bool is_afor(const gc_encode_params* p) { return p->codec == GC_GROUP_AFOR; }
+bool is_gs(const gc_encode_params* p) { return p->codec == GC_GROUP_SIMPLE; }
 gc_status refuse(const gc_encode_params* p) {
   if (!p) return GC_ERR_INVALID_ARGUMENT;
   if (p->codec != GC_GROUP_PFD && p->codec != GC_GROUP_SCHEME) return GC_ERR_UNKNOWN_CODEC;
   return GC_ERR_BAD_VARIANT;
+}
+struct GsWs {
+  uint64_t cb, nv, quad_off, M, sel, cov, idx, sums, bytes;
+};
+inline GsWs gs_ws_layout(uint64_t n_lists, uint64_t total) {
+  auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
+  const uint64_t nq = total / 4 + n_lists + 1;
+  GsWs L;
+  L.cb = 0;
+  L.nv = al(8 * (n_lists + 1));
+  L.quad_off = L.nv + al(8 * (n_lists + 1));
+  L.M = L.quad_off + al(8 * (n_lists + 1));
+  L.sel = L.M + al(4 * nq);
+  L.cov = L.sel + al(nq);
+  L.idx = L.cov + al(nq);
+  L.sums = L.idx + al(4 * nq);
+  L.bytes = L.sums + al(8 * ((n_lists + 1) / kScanB + 3));
+  return L;
+}
+GsEnc make_gs(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists, int delta,
+              uint64_t* out_off, void* ws, uint64_t total) {
+  const GsWs L = gs_ws_layout(n_lists, total);
+  GsEnc E;
+  E.values = values;
+  E.list_n = list_n;
+  E.n_lists = n_lists;
+  E.delta = delta;
+  E.out_off = out_off;
+  E.cb = (uint64_t*)((uint8_t*)ws + L.cb);
+  E.nv = (uint64_t*)((uint8_t*)ws + L.nv);
+  E.quad_off = (uint64_t*)((uint8_t*)ws + L.quad_off);
+  E.M = (uint32_t*)((uint8_t*)ws + L.M);
+  E.n_quads = 0;
+  return E;
+}
+Afor make_afor(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists, int delta,
+               uint64_t* out_off, void* ws, uint64_t total) {
+  const AforWs L = afor_ws_layout(n_lists, total);
+  uint8_t* w = (uint8_t*)ws;
+  Afor A;
+  A.values = values;
+  A.list_n = list_n;
+  A.n_lists = n_lists;
+  A.delta = delta;
+  A.out_off = out_off;
+  A.blk_off = (uint64_t*)(w + L.blk_off);
+  A.n_blocks = 0;
+  A.bmax = w + L.bmax;
+  A.fstart = w + L.fstart;
+  A.fbw = w + L.fbw;
+  A.fvec = (uint32_t*)(w + L.fvec);
+  A.fidx = (uint32_t*)(w + L.fidx);
+  A.cost = (uint64_t*)(w + L.cost);
+  A.nf = (uint64_t*)(w + L.nf);
+  A.nv = (uint64_t*)(w + L.nv);
+  return A;
 }
 Gsc make_gsc(const gc_encode_params* p, const uint32_t* values, const uint32_t* list_n,
              uint64_t n_lists, int delta, uint64_t* out_off, void* ws, uint64_t total) {
@@ -569,6 +913,8 @@ gc_status gc_encode_device_ws_size(const gc_encode_params* p, uint64_t n_lists, 
   if (!p || !bytes) return GC_ERR_INVALID_ARGUMENT;
   if (is_pfd(p)) *bytes = ws_layout(n_lists, total_ints, p->pfd_frame_quads).bytes;
   else if (is_gsc(p)) *bytes = gsc_ws_layout(n_lists, total_ints).bytes;
+  else if (is_afor(p)) *bytes = afor_ws_layout(n_lists, total_ints).bytes;
+  else if (is_gs(p)) *bytes = gs_ws_layout(n_lists, total_ints).bytes;
   else return refuse(p);
   return GC_OK;
 }
@@ -617,6 +963,89 @@ static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, con
   return GC_OK;
 }
 
+static gc_status gs_plan(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists,
+                         uint64_t total_ints, int delta, uint64_t* ctrl_off, uint64_t* data_off,
+                         uint64_t* exc_off, uint64_t* out_off, void* ws, uint64_t* sizes,
+                         cudaStream_t st) {
+  const GsWs L = gs_ws_layout(n_lists, total_ints);
+  GsEnc E = make_gs(values, list_n, n_lists, delta, out_off, ws, total_ints);
+  uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
+  if (scan_u64(GetListN{list_n}, n_lists, out_off, sums, st) != cudaSuccess ||
+      scan_u64(GetQuads{list_n}, n_lists, E.quad_off, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  uint64_t tot = 0, nq = 0;
+  if (cudaMemcpyAsync(&tot, out_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&nq, E.quad_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  if (tot != total_ints) return GC_ERR_INVALID_ARGUMENT;
+  E.n_quads = nq;
+  uint8_t* w = (uint8_t*)ws;
+  uint32_t* idx = (uint32_t*)(w + L.idx);
+  if (nq) {
+    k_gs_qmax<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(E);
+    k_gs_step<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(E, w + L.sel, w + L.cov);
+    if (cudaMemsetAsync(idx, 0xFF, 4 * nq, st) != cudaSuccess) return GC_ERR_CUDA;
+  }
+  if (n_lists) k_gs_chase<<<(unsigned)((n_lists + 127) / 128), 128, 0, st>>>(E, w + L.cov, idx);
+  if (scan_u64(GetArr{E.cb}, n_lists, E.cb, sums, st) != cudaSuccess ||
+      scan_u64(GetArr{E.nv}, n_lists, E.nv, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  const unsigned nbl = (unsigned)((n_lists + 1 + 255) / 256);
+  k_copy_u64<<<nbl, 256, 0, st>>>(E.cb, ctrl_off, n_lists + 1);
+  k_copy_u64<<<nbl, 256, 0, st>>>(E.nv, data_off, n_lists + 1);
+  if (cudaMemsetAsync(exc_off, 0, 8 * (n_lists + 1), st) != cudaSuccess) return GC_ERR_CUDA;
+  uint64_t ct = 0, vt = 0;
+  if (cudaMemcpyAsync(&ct, E.cb + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&vt, E.nv + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  sizes[0] = 16 * ((ct + 15) / 16);
+  sizes[1] = vt;
+  sizes[2] = 0;
+  sizes[3] = nq;
+  return GC_OK;
+}
+
+static gc_status afor_plan(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists,
+                           uint64_t total_ints, int delta, uint64_t* ctrl_off, uint64_t* data_off,
+                           uint64_t* exc_off, uint64_t* out_off, void* ws, uint64_t* sizes,
+                           cudaStream_t st) {
+  const AforWs L = afor_ws_layout(n_lists, total_ints);
+  Afor A = make_afor(values, list_n, n_lists, delta, out_off, ws, total_ints);
+  uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
+  if (scan_u64(GetListN{list_n}, n_lists, out_off, sums, st) != cudaSuccess ||
+      scan_u64(GetBlocks{list_n}, n_lists, A.blk_off, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  uint64_t nb = 0, tot = 0;
+  if (cudaMemcpyAsync(&nb, A.blk_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&tot, out_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  if (tot != total_ints) return GC_ERR_INVALID_ARGUMENT;
+  A.n_blocks = nb;
+  if (nb) k_afor_bmax<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(A);
+  if (n_lists) k_afor_dp<<<(unsigned)((n_lists + 127) / 128), 128, 0, st>>>(A);
+  // the per-list sizes become the list offsets (exclusive scans in place)
+  if (scan_u64(GetArr{A.nf}, n_lists, A.nf, sums, st) != cudaSuccess ||
+      scan_u64(GetArr{A.nv}, n_lists, A.nv, sums, st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  const unsigned nbl = (unsigned)((n_lists + 1 + 255) / 256);
+  k_copy_u64<<<nbl, 256, 0, st>>>(A.nf, ctrl_off, n_lists + 1);
+  k_copy_u64<<<nbl, 256, 0, st>>>(A.nv, data_off, n_lists + 1);
+  if (cudaMemsetAsync(exc_off, 0, 8 * (n_lists + 1), st) != cudaSuccess) return GC_ERR_CUDA;
+  uint64_t ct = 0, vt = 0;
+  if (cudaMemcpyAsync(&ct, A.nf + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&vt, A.nv + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  sizes[0] = 16 * ((ct + 15) / 16);
+  sizes[1] = vt;
+  sizes[2] = 0;
+  sizes[3] = nb;
+  return GC_OK;
+}
+
 gc_status gc_encode_device_plan(const gc_encode_params* p, const uint32_t* values,
                                 const uint32_t* list_n, uint64_t n_lists, uint64_t total_ints,
                                 int delta, uint64_t* ctrl_off, uint64_t* data_off,
@@ -633,6 +1062,12 @@ gc_status gc_encode_device_plan(const gc_encode_params* p, const uint32_t* value
   if (is_gsc(p))
     return gsc_plan(p, values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
                     out_off, ws, sizes, st);
+  if (is_afor(p))
+    return afor_plan(values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
+                     out_off, ws, sizes, st);
+  if (is_gs(p))
+    return gs_plan(values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
+                   out_off, ws, sizes, st);
   const WsLayout L = ws_layout(n_lists, total_ints, p->pfd_frame_quads);
   Dir D = make_dir(p, values, list_n, n_lists, delta, out_off, ws, total_ints);
   uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
@@ -693,6 +1128,28 @@ gc_status gc_encode_device_write(const gc_encode_params* p, const uint32_t* valu
       k_gsc_write<<<(unsigned)((G.n_quads + 255) / 256), 256, 0, st>>>(
           G, (const uint64_t*)((uint8_t*)ws + L.c_off), (const uint64_t*)((uint8_t*)ws + L.d_off),
           ctrl, (uint32_t*)data);
+    return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  }
+  if (is_gs(p)) {
+    const GsWs L = gs_ws_layout(n_lists, total_ints);
+    GsEnc E = make_gs(values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);
+    E.n_quads = sizes[3];
+    uint8_t* w = (uint8_t*)ws;
+    if (E.n_quads)
+      k_gs_write<<<(unsigned)((E.n_quads + 255) / 256), 256, 0, st>>>(
+          E, w + L.sel, w + L.cov, (const uint32_t*)(w + L.idx), ctrl, (uint4*)data);
+    return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  }
+  if (is_afor(p)) {
+    const AforWs L = afor_ws_layout(n_lists, total_ints);
+    Afor A = make_afor(values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);
+    A.n_blocks = sizes[3];
+    if (A.n_blocks) {
+      const uint64_t blocks = (A.n_blocks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+      k_afor_write<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(
+          A, (const uint64_t*)((uint8_t*)ws + L.nf), (const uint64_t*)((uint8_t*)ws + L.nv), ctrl,
+          (uint4*)data);
+    }
     return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
   }
   Dir D = make_dir(p, values, list_n, n_lists, delta, const_cast<uint64_t*>(out_off), ws, total_ints);

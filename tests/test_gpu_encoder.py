@@ -125,10 +125,56 @@ def test_group_scheme_docids():
     check_gsc(w.values, w.list_n, O.gsc_variant(4, "CU"), delta=True)
 
 
+def check_stream_codec(values, list_n, codec, variant=0, delta=False):
+    ref = O.encode_batch(values, list_n, codec, variant, delta=delta, threads=8)
+    v = torch.from_numpy(np.ascontiguousarray(values, np.uint32).view(np.int32)).cuda()
+    ln = torch.from_numpy(np.ascontiguousarray(list_n, np.uint32).view(np.int32)).cuda()
+    db = gc.encode_device(v, ln, codec, variant, delta=delta)
+    torch.cuda.synchronize()
+    t = db.tensors
+    for k in KEYS:
+        assert np.array_equal(t[k].cpu().numpy().view(np.uint64), ref[k]), k
+    assert np.array_equal(t["ctrl"].cpu().numpy(), ref["ctrl"])
+    assert np.array_equal(t["data"].cpu().numpy().view(np.uint32).reshape(-1, 4), ref["data"])
+    out, ws = gc.decode_dgaps(db)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) == 0
+    assert np.array_equal(out[:db.total_out].cpu().numpy().view(np.uint32),
+                          O.decode_batch(ref, dgaps=True, threads=8))
+
+
+def test_group_afor_random():
+    """Group-AFOR (the DP of A23-A25) encoded on the device, lists in parallel."""
+    rng = np.random.default_rng(91)
+    for n_lists, max_len, bits, spike in ((1, 5, 2, 0.0), (80, 2000, 10, 0.05),
+                                          (500, 600, 6, 0.02), (10, 30000, 24, 0.001),
+                                          (30, 300, 32, 0.0)):
+        w = gen.random_lists(rng, n_lists, max_len, bits, spike)
+        check_stream_codec(w.values, w.list_n, O.GROUP_AFOR)
+    w = gen.config(1)
+    check_stream_codec(w.values, w.list_n, O.GROUP_AFOR, delta=True)
+
+
+def test_group_afor_config4_full_size():
+    """BASELINE config 4 at full size (2^29 gaps in 10^6 lists)."""
+    w = gen.config(4)
+    check_stream_codec(w.values, w.list_n, O.GROUP_AFOR)
+
+
+def test_group_simple():
+    """Group-Simple (Algorithm 1) encoded on the device, lists in parallel."""
+    rng = np.random.default_rng(93)
+    for n_lists, max_len, bits, spike in ((1, 3, 1, 0.0), (100, 1500, 8, 0.03),
+                                          (400, 200, 3, 0.0), (20, 5000, 32, 0.0)):
+        w = gen.random_lists(rng, n_lists, max_len, bits, spike)
+        check_stream_codec(w.values, w.list_n, O.GROUP_SIMPLE)
+    w = gen.config(1)  # BASELINE config 1 at full size, docIDs in
+    check_stream_codec(w.values, w.list_n, O.GROUP_SIMPLE, delta=True)
+
+
 def test_other_codecs_refused():
     v = torch.zeros(16, dtype=torch.int32, device="cuda")
     ln = torch.tensor([16], dtype=torch.int32, device="cuda")
-    for codec, variant in ((gc.GROUP_SCHEME, O.gsc_variant(8, "IU")), (gc.GROUP_AFOR, 0),
-                           (gc.GROUP_SIMPLE, 0)):
+    for codec, variant in ((gc.GROUP_SCHEME, O.gsc_variant(8, "IU")), (7, 0)):
         with pytest.raises(gc.GcError):
             gc.encode_device(v, ln, codec, variant)
