@@ -214,8 +214,8 @@ def run_reference(args, rank, world):
 
 def run_encode(args, dev):
     """--encode: the GPU encoders on the config's inputs resident in HBM:
-    config 1 -> Group-Simple (docIDs in), config 2 -> Group-Scheme binary + complete unary
-    (8 variants), config 3 -> Group-PFD and SIMD-BP128, config 4 -> Group-AFOR.  ints/s per codec (gc_encode_device_plan + _write, events on the stream; plan
+    config 1 -> Group-Simple (docIDs in), config 2 -> Group-Scheme (all 10 variants),
+    config 3 -> Group-PFD and SIMD-BP128, config 4 -> Group-AFOR.  ints/s per codec (gc_encode_device_plan + _write, events on the stream; plan
     reads the stream sizes back, a host sync), with the oracle encoder on the host cores
     beside it (bounded sample)."""
     import torch
@@ -226,8 +226,7 @@ def run_encode(args, dev):
     w = gen.config(k, scale=args.scale)
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
     if k == 2:
-        codecs = [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd)) for cg, kd in gc.GSC_VARIANTS
-                  if kd != "IU"]
+        codecs = [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd)) for cg, kd in gc.GSC_VARIANTS]
     elif k == 3:
         codecs = [(gc.GROUP_PFD, 0), (gc.GROUP_PFD, 1)]
     else:

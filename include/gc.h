@@ -205,11 +205,11 @@ void gc_encode_abort(void* handle);
 
 /* ---------------------------------------------------------------------------
  * GPU encoders: Group-Simple (Algorithm 1),
- * Group-Scheme with binary or complete unary LD, Group-AFOR,
+ * Group-Scheme, all 10 variants, Group-AFOR,
  * Group-PFD (variant 0) and SIMD-BP128 (PFD variant 1); bytes
- * identical to the host encoder's and the oracle's.  Group-Scheme IU:
- * GC_ERR_BAD_VARIANT (use the host encoder).  sizes[3] is an internal count (frames,
- * quads or blocks): pass sizes back to gc_encode_device_write unchanged.  All arrays are DEVICE memory except sizes[] and the
+ * identical to the host encoder's and the oracle's (every codec and variant the
+ * decoder takes; an invalid variant: GC_ERR_BAD_VARIANT).  sizes[3] is an internal
+ * count (frames, quads or blocks): pass sizes back to gc_encode_device_write unchanged.  All arrays are DEVICE memory except sizes[] and the
  * params struct.
  *   values[total_ints], list_n[n_lists]  as for gc_encode_begin (docIDs if delta)
  *   ws, ws_bytes         workspace of at least gc_encode_device_ws_size bytes,

@@ -399,8 +399,25 @@ __global__ void k_gsc_sizes(Gsc G, uint64_t* cb, uint64_t* vecs) {
   } else {  // A18: CG 1 three 5-bit fields per 16-bit unit, CG 2/4 two per byte, CG 8 four
     bytes = G.cg == 1 ? 2 * ((Q + 2) / 3) : (G.cg == 8 ? (Q + 3) / 4 : (Q + 1) / 2);
   }
-  cb[l] = 4 * ((bytes + 3) / 4);
+  if (G.kind != 2) cb[l] = 4 * ((bytes + 3) / 4);  // (IU: k_gsc_iu_pos)
   vecs[l] = (G.bw_off[qe] - G.bw_off[qs] + 31) / 32;
+}
+// incomplete unary (A17): a code never crosses a byte -- if it does not fit in the rest of
+// the current byte, that rest is filled with 1s and the code starts the next byte; the last
+// byte is filled with 1s too.  One thread per list walks its codes (a sequential state);
+// cu_off[g] = the code's bit position within the list's control area.
+__global__ void k_gsc_iu_pos(Gsc G, uint64_t* cb) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= G.n_lists) return;
+  uint64_t p = 0;
+  for (uint64_t g = G.quad_off[l]; g < G.quad_off[l + 1]; g++) {
+    const uint32_t u = G.u[g], used = (uint32_t)(p & 7);
+    if (used != 0 && used + u > 8) p = (p + 7) & ~7ull;
+    G.cu_off[g] = p;
+    p += u;
+  }
+  const uint64_t bytes = (p + 7) / 8;
+  cb[l] = 4 * ((bytes + 3) / 4);
 }
 __device__ __forceinline__ void or_byte_bits(uint8_t* base, uint64_t byte, uint32_t bits) {
   // OR `bits` (8 bits) into the byte at `byte` through its aligned 32-bit word
@@ -416,15 +433,22 @@ __global__ void k_gsc_write(Gsc G, const uint64_t* ctrl_off, const uint64_t* dat
   const uint32_t u = G.u[g], bw = G.cg * u;
   // control
   const uint64_t cbase = ctrl_off[l];
-  if (G.kind == 1) {  // (u-1) ones then a 0, MSB-first in address order
-    const uint64_t c = G.cu_off[g] - G.cu_off[qs];
-    for (uint64_t i = c; i + 1 < c + u;) {  // the ones, a byte at a time
-      const uint64_t byte = i >> 3;
-      const uint64_t e = c + u - 1 - 8 * byte;
-      const uint32_t b0 = (uint32_t)(i & 7), b1 = e < 8 ? (uint32_t)e : 8u;
-      const uint32_t bits = ((0xFFu >> b0) & ~(0xFFu >> b1)) & 0xFFu;  // bits b0..b1-1 from the MSB
-      or_byte_bits(ctrl, cbase + byte, bits);
-      i = 8 * byte + b1;
+  if (G.kind >= 1) {  // (u-1) ones then a 0, MSB-first in address order
+    const uint64_t c = G.kind == 1 ? G.cu_off[g] - G.cu_off[qs] : G.cu_off[g];
+    auto ones = [&](uint64_t from, uint64_t to) {  // stream bits [from, to) set, a byte at a time
+      for (uint64_t i = from; i < to;) {
+        const uint64_t byte = i >> 3;
+        const uint64_t e = to - 8 * byte;
+        const uint32_t b0 = (uint32_t)(i & 7), b1 = e < 8 ? (uint32_t)e : 8u;
+        or_byte_bits(ctrl, cbase + byte, ((0xFFu >> b0) & ~(0xFFu >> b1)) & 0xFFu);
+        i = 8 * byte + b1;
+      }
+    };
+    ones(c, c + u - 1);
+    if (G.kind == 2) {  // IU: the 1s that fill the byte up to the next code (or its end)
+      const uint64_t end = c + u;
+      const uint64_t next = g + 1 < G.quad_off[l + 1] ? G.cu_off[g + 1] : (end + 7) & ~7ull;
+      ones(end, next);
     }
   } else {
     const uint32_t f = u - 1;  // A13: binary stores u - 1
@@ -797,9 +821,9 @@ bool is_pfd(const gc_encode_params* p) {
   return p->codec == GC_GROUP_PFD && (p->pfd_frame_quads == 32 || p->pfd_frame_quads == 128) &&
          p->variant <= 1 && (p->variant == 1 || p->zeta_den > 0);
 }
-bool is_gsc(const gc_encode_params* p) {  // binary or complete unary (IU: host encoder)
-  const uint32_t kind = (p->variant >> 2) & 3u;
-  return p->codec == GC_GROUP_SCHEME && p->variant <= 15 && kind <= 1;
+bool is_gsc(const gc_encode_params* p) {  // binary, complete unary, incomplete unary (CG 4/8)
+  const uint32_t kind = (p->variant >> 2) & 3u, cg = 1u << (p->variant & 3u);
+  return p->codec == GC_GROUP_SCHEME && p->variant <= 15 && kind <= 2 && !(kind == 2 && cg < 4);
 }
 bool is_afor(const gc_encode_params* p) { return p->codec == GC_GROUP_AFOR; }
 bool is_gs(const gc_encode_params* p) { return p->codec == GC_GROUP_SIMPLE; }
@@ -942,6 +966,7 @@ static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, con
   if (nq) k_gsc_units<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(G);
   if (scan_u64(GetBW{G.u, G.cg}, nq, G.bw_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
   if (G.kind == 1 && scan_u64(GetU{G.u}, nq, G.cu_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (G.kind == 2 && n_lists) k_gsc_iu_pos<<<(unsigned)((n_lists + 127) / 128), 128, 0, st>>>(G, c_off);
   if (n_lists) k_gsc_sizes<<<(unsigned)((n_lists + 255) / 256), 256, 0, st>>>(G, c_off, d_off);
   // exclusive scans in place: the per-list sizes become the list offsets
   if (scan_u64(GetArr{c_off}, n_lists, c_off, sums, st) != cudaSuccess ||

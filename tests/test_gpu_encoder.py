@@ -80,7 +80,7 @@ def test_config3_full_size(variant):
     check(w.values, w.list_n, variant, 32)
 
 
-GSC_BCU = [(cg, k) for cg in (1, 2, 4, 8) for k in ("B", "CU")]
+GSC_BCU = [(cg, k) for cg in (1, 2, 4, 8) for k in ("B", "CU")] + [(4, "IU"), (8, "IU")]
 
 
 def check_gsc(values, list_n, variant, delta=False):
@@ -104,7 +104,8 @@ def check_gsc(values, list_n, variant, delta=False):
 
 @pytest.mark.parametrize("cg,kind", GSC_BCU, ids=[f"GSC-{c}-{k}" for c, k in GSC_BCU])
 def test_group_scheme_random(cg, kind):
-    """Group-Scheme binary / complete unary encoded on the device."""
+    """Group-Scheme binary / complete unary / incomplete unary encoded on the
+    device."""
     rng = np.random.default_rng(70 + cg + (kind == "CU"))
     variant = O.gsc_variant(cg, kind)
     for n_lists, max_len, bits, spike in ((1, 6, 3, 0.0), (60, 900, 11, 0.05),
@@ -114,7 +115,7 @@ def test_group_scheme_random(cg, kind):
 
 
 def test_group_scheme_config2_full_size():
-    """BASELINE config 2 at full size (2^26 gaps in 10^5 lists), every B / CU variant."""
+    """BASELINE config 2 at full size (2^26 gaps in 10^5 lists), all 10 variants."""
     w = gen.config(2)
     for cg, kind in GSC_BCU:
         check_gsc(w.values, w.list_n, O.gsc_variant(cg, kind))
@@ -175,6 +176,6 @@ def test_group_simple():
 def test_other_codecs_refused():
     v = torch.zeros(16, dtype=torch.int32, device="cuda")
     ln = torch.tensor([16], dtype=torch.int32, device="cuda")
-    for codec, variant in ((gc.GROUP_SCHEME, O.gsc_variant(8, "IU")), (7, 0)):
+    for codec, variant in ((gc.GROUP_SCHEME, 2 << 2), (7, 0)):  # (IU needs CG 4 or 8)
         with pytest.raises(gc.GcError):
             gc.encode_device(v, ln, codec, variant)
