@@ -404,20 +404,71 @@ __global__ void k_gsc_sizes(Gsc G, uint64_t* cb, uint64_t* vecs) {
 }
 // incomplete unary (A17): a code never crosses a byte -- if it does not fit in the rest of
 // the current byte, that rest is filled with 1s and the code starts the next byte; the last
-// byte is filled with 1s too.  One thread per list walks its codes (a sequential state);
-// cu_off[g] = the code's bit position within the list's control area.
-__global__ void k_gsc_iu_pos(Gsc G, uint64_t* cb) {
+// byte is filled with 1s too.  The placement is a sequential state per list (bits used in
+// the current byte, 0..7), so lists are cut into chunks of kIuChunk quads: every chunk's
+// bit advance for each of the 8 entry states (in parallel), one thread per list chains its
+// chunks, then every chunk places its codes from its entry position (cu_off[g] = the code's
+// bit position within the list's control area).
+constexpr uint32_t kIuChunk = 256;
+struct GetIuChunks {
+  const uint64_t* quad_off;
+  __device__ uint64_t operator()(uint64_t i) const {
+    return (quad_off[i + 1] - quad_off[i] + kIuChunk - 1) / kIuChunk;
+  }
+};
+__device__ __forceinline__ uint64_t iu_walk(const Gsc& G, uint64_t g0, uint64_t g1, uint64_t p,
+                                            uint64_t* pos) {
+  for (uint64_t g = g0; g < g1; g++) {
+    const uint32_t u = G.u[g], used = (uint32_t)(p & 7);
+    if (used != 0 && used + u > 8) p = (p + 7) & ~7ull;
+    if (pos) pos[g] = p;
+    p += u;
+  }
+  return p;
+}
+struct IuChunk {
+  const uint64_t* ch_off;  // [L+1] first chunk of each list
+  uint64_t n_chunks;
+  uint32_t* adv;           // [n_chunks][8] bit advance from entry state s
+  uint64_t* start;         // [n_chunks] entry position (bits from the list's start)
+};
+__device__ __forceinline__ uint64_t list_of_chunk(const Gsc& G, const IuChunk& K, uint64_t c) {
+  uint64_t a = 0, b = G.n_lists;
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (K.ch_off[m] <= c) a = m;
+    else b = m;
+  }
+  return a;
+}
+__global__ void k_iu_adv(Gsc G, IuChunk K) {  // thread = (chunk, entry state)
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 8 * K.n_chunks) return;
+  const uint64_t c = t >> 3;
+  const uint32_t st = (uint32_t)(t & 7);
+  const uint64_t l = list_of_chunk(G, K, c);
+  const uint64_t g0 = G.quad_off[l] + (c - K.ch_off[l]) * kIuChunk;
+  const uint64_t g1 = min(g0 + kIuChunk, G.quad_off[l + 1]);
+  K.adv[t] = (uint32_t)(iu_walk(G, g0, g1, st, nullptr) - st);
+}
+__global__ void k_iu_chain(Gsc G, IuChunk K, uint64_t* cb) {  // thread = list
   const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= G.n_lists) return;
   uint64_t p = 0;
-  for (uint64_t g = G.quad_off[l]; g < G.quad_off[l + 1]; g++) {
-    const uint32_t u = G.u[g], used = (uint32_t)(p & 7);
-    if (used != 0 && used + u > 8) p = (p + 7) & ~7ull;
-    G.cu_off[g] = p;
-    p += u;
+  for (uint64_t c = K.ch_off[l]; c < K.ch_off[l + 1]; c++) {
+    K.start[c] = p;
+    p += K.adv[8 * c + (p & 7)];
   }
   const uint64_t bytes = (p + 7) / 8;
   cb[l] = 4 * ((bytes + 3) / 4);
+}
+__global__ void k_iu_place(Gsc G, IuChunk K) {  // thread = chunk
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K.n_chunks) return;
+  const uint64_t l = list_of_chunk(G, K, c);
+  const uint64_t g0 = G.quad_off[l] + (c - K.ch_off[l]) * kIuChunk;
+  const uint64_t g1 = min(g0 + kIuChunk, G.quad_off[l + 1]);
+  iu_walk(G, g0, g1, K.start[c], G.cu_off);
 }
 __device__ __forceinline__ void or_byte_bits(uint8_t* base, uint64_t byte, uint32_t bits) {
   // OR `bits` (8 bits) into the byte at `byte` through its aligned 32-bit word
@@ -786,7 +837,7 @@ __global__ void k_gs_write(GsEnc E, const uint8_t* sel, const uint8_t* cov, cons
 }
 
 struct GscWs {
-  uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, sums, bytes;
+  uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, ch_off, adv, start, sums, bytes;
 };
 inline GscWs gsc_ws_layout(uint64_t n_lists, uint64_t total) {
   auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
@@ -799,7 +850,11 @@ inline GscWs gsc_ws_layout(uint64_t n_lists, uint64_t total) {
   L.cu_off = L.bw_off + al(8 * (nq + 1));
   L.c_off = L.cu_off + al(8 * (nq + 1));
   L.d_off = L.c_off + al(8 * (n_lists + 1));
-  L.sums = L.d_off + al(8 * (n_lists + 1));
+  const uint64_t nch = nq / kIuChunk + n_lists + 1;  // IU chunks
+  L.ch_off = L.d_off + al(8 * (n_lists + 1));
+  L.adv = L.ch_off + al(8 * (n_lists + 1));
+  L.start = L.adv + al(32 * nch);
+  L.sums = L.start + al(8 * nch);
   L.bytes = L.sums + al(8 * (nsum + 1));
   return L;
 }
@@ -966,7 +1021,22 @@ static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, con
   if (nq) k_gsc_units<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(G);
   if (scan_u64(GetBW{G.u, G.cg}, nq, G.bw_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
   if (G.kind == 1 && scan_u64(GetU{G.u}, nq, G.cu_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
-  if (G.kind == 2 && n_lists) k_gsc_iu_pos<<<(unsigned)((n_lists + 127) / 128), 128, 0, st>>>(G, c_off);
+  if (G.kind == 2 && n_lists) {
+    IuChunk K;
+    K.ch_off = (uint64_t*)(w + L.ch_off);
+    K.adv = (uint32_t*)(w + L.adv);
+    K.start = (uint64_t*)(w + L.start);
+    if (scan_u64(GetIuChunks{G.quad_off}, n_lists, const_cast<uint64_t*>(K.ch_off), sums, st) != cudaSuccess)
+      return GC_ERR_CUDA;
+    uint64_t nch = 0;
+    if (cudaMemcpyAsync(&nch, K.ch_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return GC_ERR_CUDA;
+    K.n_chunks = nch;
+    if (nch) k_iu_adv<<<(unsigned)((8 * nch + 255) / 256), 256, 0, st>>>(G, K);
+    k_iu_chain<<<(unsigned)((n_lists + 127) / 128), 128, 0, st>>>(G, K, c_off);
+    if (nch) k_iu_place<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(G, K);
+  }
   if (n_lists) k_gsc_sizes<<<(unsigned)((n_lists + 255) / 256), 256, 0, st>>>(G, c_off, d_off);
   // exclusive scans in place: the per-list sizes become the list offsets
   if (scan_u64(GetArr{c_off}, n_lists, c_off, sums, st) != cudaSuccess ||
