@@ -8,12 +8,19 @@
 
 namespace gcd {
 
-constexpr int kThreads = 256;
+#ifndef GC_ITHREADS
+#define GC_ITHREADS 256
+#endif
+#ifndef GC_WA
+#define GC_WA 2048
+#endif
+constexpr int kThreads = GC_ITHREADS;  // index / list kernels
 constexpr int kWarps = kThreads / 32;
 
 // Index kernel (control-space tiles): 2048 control words, 8 per thread.
-constexpr uint32_t kWA = 2048;
+constexpr uint32_t kWA = GC_WA;
 constexpr uint32_t kCA = kWA / kThreads;
+static_assert(kCA == 8, "the index kernel parses 8 control words per thread");
 
 // Decode kernel (output-space tiles): tile t owns the output ints
 // [t*kT, (t+1)*kT) exactly; it decodes every quadruple that holds one of them.

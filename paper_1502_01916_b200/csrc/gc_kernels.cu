@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   __shared__ Seg4 s_scr[kWarps];
   __shared__ uint32_t s_tile, s_err, s_nq, s_nl, s_nw, s_lastli, s_pq;
   __shared__ unsigned long long s_la, s_pd, s_pe;
-  constexpr uint32_t kQueue = 384;  // words needing a group walk (list ends, suspicious words)
+  constexpr uint32_t kQueue = 3 * kThreads / 2;  // words needing a group walk (list ends, suspicious)
   __shared__ uint32_t s_qw[kQueue], s_qi[kQueue], s_qq[kQueue];
   __shared__ unsigned long long s_qd[kQueue], s_qe[C::kExc ? kQueue : 1];
   const uint32_t tid = threadIdx.x, lane = tid & 31;
