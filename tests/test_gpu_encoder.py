@@ -179,3 +179,39 @@ def test_other_codecs_refused():
     for codec, variant in ((gc.GROUP_SCHEME, 2 << 2), (7, 0)):  # (IU needs CG 4 or 8)
         with pytest.raises(gc.GcError):
             gc.encode_device(v, ln, codec, variant)
+
+
+ALL_CODECS = ([(O.GROUP_SIMPLE, 0), (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0), (O.GROUP_PFD, 1)]
+              + [(O.GROUP_SCHEME, O.gsc_variant(cg, k)) for cg, k in GSC_BCU])
+
+
+@pytest.mark.parametrize("codec,variant", ALL_CODECS,
+                         ids=[gc.codec_label(c, v) for c, v in ALL_CODECS])
+def test_edge_batches(codec, variant):
+    """Every GPU encoder on the edge shapes: all-empty lists, 1-int lists, all-zero and
+    all-max values, a long single list, empty lists at the end."""
+    rng = np.random.default_rng(11)
+    cases = [
+        (np.zeros(5, np.uint32), np.zeros(0, np.uint32)),
+        (np.ones(700, np.uint32), rng.integers(0, 1 << 32, 700, dtype=np.uint64).astype(np.uint32)),
+        (np.array([0, 3, 0, 4096, 1, 4095, 4097, 0, 0], np.uint32), None),
+        (np.array([70000], np.uint32), np.zeros(70000, np.uint32)),
+        (np.array([5000, 3], np.uint32), np.full(5003, 0xFFFFFFFF, np.uint32)),
+    ]
+    for ln, vals in cases:
+        if vals is None:
+            vals = rng.integers(0, 1 << 13, int(ln.sum()), dtype=np.uint64).astype(np.uint32)
+        if codec == O.GROUP_PFD:
+            check(vals, ln, variant, 32)
+        elif codec == O.GROUP_SCHEME:
+            check_gsc(vals, ln, variant)
+        else:
+            check_stream_codec(vals, ln, codec, variant)
+
+
+def test_empty_batch():
+    v = torch.zeros(0, dtype=torch.int32, device="cuda")
+    ln = torch.zeros(0, dtype=torch.int32, device="cuda")
+    for codec, variant in ALL_CODECS:
+        db = gc.encode_device(v, ln, codec, variant)
+        assert db.total_out == 0 and db.data_vectors == 0 and db.ctrl_bytes == 0
