@@ -342,7 +342,21 @@ struct Gsc {
   uint8_t* u;              // [n_quads] units per quad
   uint64_t* bw_off;        // [n_quads+1] exclusive scan of BW (lane bits)
   uint64_t* cu_off;        // [n_quads+1] exclusive scan of u (CU control bits)
+  uint32_t* lstart;        // [n_quads] lists starting at each quad (list ids >= 1)
+  uint64_t* lid;           // [n_quads+1] exclusive scan of lstart: lid[g+1] = list of quad g
 };
+struct GetStarts {
+  const uint32_t* p;
+  __device__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+// lstart[quad_off[l]] += 1 for every list l >= 1 (empty lists share their successor's start),
+// so the inclusive scan at quad g counts the lists starting at or before g: g's list
+__global__ void k_gsc_lstart(Gsc G) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (l >= G.n_lists) return;
+  const uint64_t q = G.quad_off[l];
+  if (q < G.n_quads) atomicAdd(&G.lstart[q], 1u);
+}
 struct GetQuads {
   const uint32_t* list_n;
   __device__ uint64_t operator()(uint64_t i) const { return (list_n[i] + 3ull) >> 2; }
@@ -365,6 +379,11 @@ __device__ __forceinline__ uint64_t list_of_quad(const Gsc& G, uint64_t g) {
   }
   return a;
 }
+// the list of quad g for a full warp of consecutive quads: one binary search (lane 0, the
+// warp's first quad), then every lane steps forward over the few list starts in between
+__device__ __forceinline__ uint64_t warp_list_of_quad(const Gsc& G, uint64_t g) {
+  return g < G.n_quads ? G.lid[g + 1] : 0;  // (precomputed, no search)
+}
 __device__ __forceinline__ void gsc_quad(const Gsc& G, uint64_t l, uint64_t j, uint32_t* v) {
   const uint32_t n = G.list_n[l];
   const uint64_t e = G.out_off[l] + 4 * j;
@@ -381,8 +400,8 @@ __device__ __forceinline__ void gsc_quad(const Gsc& G, uint64_t l, uint64_t j, u
 }
 __global__ void k_gsc_units(Gsc G) {
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t l = warp_list_of_quad(G, g);
   if (g >= G.n_quads) return;
-  const uint64_t l = list_of_quad(G, g);
   uint32_t v[4];
   gsc_quad(G, l, g - G.quad_off[l], v);
   const uint32_t w = width_of(v[0] | v[1] | v[2] | v[3]);  // width of the quad max (A9)
@@ -476,12 +495,11 @@ __device__ __forceinline__ void or_byte_bits(uint8_t* base, uint64_t byte, uint3
   uint32_t* w = reinterpret_cast<uint32_t*>(base + (byte & ~3ull));
   atomicOr(w, bits << (8 * (uint32_t)(byte & 3)));
 }
-__global__ void k_gsc_write(Gsc G, const uint64_t* ctrl_off, const uint64_t* data_off, uint8_t* ctrl,
-                            uint32_t* data) {
-  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= G.n_quads) return;
-  const uint64_t l = list_of_quad(G, g), qs = G.quad_off[l], j = g - qs;
-  const uint32_t u = G.u[g], bw = G.cg * u;
+// one quad's control: its binary field (A18) or its unary code (+ IU padding 1s)
+__device__ __forceinline__ void gsc_ctrl(const Gsc& G, uint64_t g, uint64_t l, const uint64_t* ctrl_off,
+                                         uint8_t* ctrl) {
+  const uint64_t qs = G.quad_off[l], j = g - qs;
+  const uint32_t u = G.u[g];
   // control
   const uint64_t cbase = ctrl_off[l];
   if (G.kind >= 1) {  // (u-1) ones then a 0, MSB-first in address order
@@ -512,26 +530,79 @@ __global__ void k_gsc_write(Gsc G, const uint64_t* ctrl_off, const uint64_t* dat
     const uint64_t a = cbase + byte;  // (a 16-bit unit never crosses its aligned word)
     atomicOr(reinterpret_cast<uint32_t*>(ctrl + (a & ~3ull)), f << (sh + 8 * (uint32_t)(a & 3)));
   }
-  // data: the 4 lane values at the quad's lane-bit position (A3 split)
-  uint32_t v[4];
-  gsc_quad(G, l, j, v);
-  const uint64_t pos = data_off[l] * 32 + (G.bw_off[g] - G.bw_off[qs]);
-  const uint64_t m = pos >> 5;
-  const uint32_t off = (uint32_t)(pos & 31), rem = 32u - off;
+}
+
+constexpr uint32_t kGscSpan = 72;  // data words a warp's 32 quads can touch (<= 65)
+__global__ void __launch_bounds__(256) k_gsc_write(Gsc G, const uint64_t* ctrl_off,
+                                                   const uint64_t* data_off, uint8_t* ctrl,
+                                                   uint32_t* data) {
+  __shared__ uint32_t s_pack[8][4 * kGscSpan];
+  const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = g < G.n_quads;
+  const uint64_t lw = warp_list_of_quad(G, g);
+  uint64_t pos = 0;
+  uint32_t bw = 0, v[4] = {0, 0, 0, 0};
+  if (act) {
+    const uint64_t l = lw, qs = G.quad_off[l];
+    bw = G.cg * G.u[g];
+    gsc_quad(G, l, g - qs, v);
+    pos = data_off[l] * 32 + (G.bw_off[g] - G.bw_off[qs]);
+    gsc_ctrl(G, g, l, ctrl_off, ctrl);
+  }
+  // data: the warp's 32 quads are consecutive in the data stream; pack them in shared
+  // memory, store the interior words, OR only the two end words a neighbour may share
+  if (__all_sync(0xffffffffu, !act)) return;
+  uint64_t m_lo = act ? (pos >> 5) : ~0ull, m_hi = act ? ((pos + bw - 1) >> 5) : 0ull;
 #pragma unroll
-  for (int t = 0; t < 4; t++) {
-    const uint32_t x = low_bits(v[t], bw);
-    if (!x) continue;
-    if (bw <= rem) {
-      atomicOr(&data[4 * m + t], x << off);
+  for (int o = 16; o > 0; o >>= 1) {
+    m_lo = min(m_lo, (uint64_t)__shfl_xor_sync(0xffffffffu, m_lo, o));
+    m_hi = max(m_hi, (uint64_t)__shfl_xor_sync(0xffffffffu, m_hi, o));
+  }
+  uint32_t* pk = s_pack[wi];
+  const uint64_t span = m_hi - m_lo + 1;
+  if (span > kGscSpan) {  // (cannot happen for 32 quads; kept for safety) -- OR directly
+    if (act) {
+      const uint64_t m = pos >> 5;
+      const uint32_t off = (uint32_t)(pos & 31), rem = 32u - off;
+      for (int t = 0; t < 4; t++) {
+        const uint32_t x = low_bits(v[t], bw);
+        if (bw <= rem) atomicOr(&data[4 * m + t], x << off);
+        else {
+          atomicOr(&data[4 * m + t], (x >> (bw - rem)) << off);
+          atomicOr(&data[4 * (m + 1) + t], low_bits(x, bw - rem));
+        }
+      }
+    }
+    return;
+  }
+  for (uint32_t w = lane; w < 4 * span; w += 32) pk[w] = 0;
+  __syncwarp();
+  if (act) {
+    const uint32_t m = (uint32_t)((pos >> 5) - m_lo), off = (uint32_t)(pos & 31), rem = 32u - off;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const uint32_t x = low_bits(v[t], bw);
+      if (!x) continue;
+      if (bw <= rem) {
+        atomicOr(&pk[4 * m + t], x << off);
+      } else {  // high part at the top of word m, low part at the bottom of word m+1 (A3)
+        atomicOr(&pk[4 * m + t], (x >> (bw - rem)) << off);
+        atomicOr(&pk[4 * (m + 1) + t], low_bits(x, bw - rem));
+      }
+    }
+  }
+  __syncwarp();
+  for (uint32_t w = lane; w < 4 * span; w += 32) {
+    const uint32_t word = w >> 2, x = pk[w];
+    uint32_t* dst = &data[4 * (m_lo + word) + (w & 3)];
+    if (word == 0 || word + 1 == span) {
+      if (x) atomicOr(dst, x);
     } else {
-      const uint32_t lo = bw - rem;
-      atomicOr(&data[4 * m + t], (x >> lo) << off);
-      atomicOr(&data[4 * (m + 1) + t], low_bits(x, lo));
+      *dst = x;
     }
   }
 }
-
 struct WsLayout {
   uint64_t frame_off, rec, vec_off, exb_off, sums, bytes;
 };
@@ -837,7 +908,7 @@ __global__ void k_gs_write(GsEnc E, const uint8_t* sel, const uint8_t* cov, cons
 }
 
 struct GscWs {
-  uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, ch_off, adv, start, sums, bytes;
+  uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, ch_off, adv, start, lstart, lid, sums, bytes;
 };
 inline GscWs gsc_ws_layout(uint64_t n_lists, uint64_t total) {
   auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
@@ -854,7 +925,9 @@ inline GscWs gsc_ws_layout(uint64_t n_lists, uint64_t total) {
   L.ch_off = L.d_off + al(8 * (n_lists + 1));
   L.adv = L.ch_off + al(8 * (n_lists + 1));
   L.start = L.adv + al(32 * nch);
-  L.sums = L.start + al(8 * nch);
+  L.lstart = L.start + al(8 * nch);
+  L.lid = L.lstart + al(4 * nq);
+  L.sums = L.lid + al(8 * (nq + 1));
   L.bytes = L.sums + al(8 * (nsum + 1));
   return L;
 }
@@ -960,6 +1033,8 @@ Gsc make_gsc(const gc_encode_params* p, const uint32_t* values, const uint32_t* 
   G.u = w + L.u;
   G.bw_off = (uint64_t*)(w + L.bw_off);
   G.cu_off = (uint64_t*)(w + L.cu_off);
+  G.lstart = (uint32_t*)(w + L.lstart);
+  G.lid = (uint64_t*)(w + L.lid);
   return G;
 }
 Dir make_dir(const gc_encode_params* p, const uint32_t* values, const uint32_t* list_n,
@@ -1018,7 +1093,12 @@ static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, con
     return GC_ERR_CUDA;
   if (tot != total_ints) return GC_ERR_INVALID_ARGUMENT;
   G.n_quads = nq;
-  if (nq) k_gsc_units<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(G);
+  if (nq) {  // the list of every quad (no per-quad search)
+    if (cudaMemsetAsync(G.lstart, 0, 4 * nq, st) != cudaSuccess) return GC_ERR_CUDA;
+    if (n_lists > 1) k_gsc_lstart<<<(unsigned)((n_lists + 255) / 256), 256, 0, st>>>(G);
+    if (scan_u64(GetStarts{G.lstart}, nq, G.lid, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+    k_gsc_units<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(G);
+  }
   if (scan_u64(GetBW{G.u, G.cg}, nq, G.bw_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
   if (G.kind == 1 && scan_u64(GetU{G.u}, nq, G.cu_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
   if (G.kind == 2 && n_lists) {
