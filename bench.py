@@ -406,10 +406,13 @@ def main():
         pg.barrier()
     torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local_rank) as clk:
         t0.record(stream)
         for k in range(args.steps):
+            step_ev[k].record(stream)
             step(ev[k])
+        step_ev[args.steps].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
     if pg:
@@ -420,6 +423,21 @@ def main():
               for i in range(len(dbs))]
     idx_ms = [sum(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)) / args.steps
               for i in range(len(dbs))]
+    step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps))
+
+    # ---- gc_decode (gaps only, the paper's measured path, A38) beside it: k_decode without
+    # the d-gap scan, same variants, same repetitions (untimed for the headline)
+    gaps_ms = []
+    for db, ws in zip(dbs, wss):
+        gc.decode_stage(db, out, ws, False, gc.STAGE_RESET | gc.STAGE_INDEX, stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.decode_stage(db, out, ws, False, gc.STAGE_DECODE, stream)  # (warm)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gc.decode_stage(db, out, ws, False, gc.STAGE_DECODE, stream)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gaps_ms.append(g0.elapsed_time(g1) / args.steps)
 
     # ---- NCCL: max time over ranks; sum of counts / checksums / status (after timing)
     status = 0
@@ -445,14 +463,17 @@ def main():
     peak, peak_src = peaks()
     traffic = ncu_traffic(w.name)
     per_codec = {}
-    for lab, hb, a, dm, im in zip(labels, hbs, algo, dec_ms, idx_ms):
+    for lab, hb, a, dm, im, gm in zip(labels, hbs, algo, dec_ms, idx_ms, gaps_ms):
         per_codec[lab] = {
             "ints_per_s": hb.total_out / ((dm + im) / 1e3),
             "decode_kernel_ms": round(dm, 5), "index_ms": round(im, 5),
             "bits_per_int": round(8 * hb.compressed_bytes / max(hb.total_out, 1), 3),
             "decode_kernel_gbs": round(a / (dm / 1e3) / 1e9, 1),
             "frac_of_peak": round(a / (dm / 1e3) / 1e9 / peak, 3),
+            "gaps_only_decode_kernel_ms": round(gm, 5),
+            "gaps_only_frac_of_peak": round(a / (gm / 1e3) / 1e9 / peak, 3),
         }
+    gaps_achieved = sum(algo) / (sum(gaps_ms) / 1e3) / 1e9
 
     # ---- e2e through the C ABI from pinned HOST buffers (copies inside the timed region)
     e2e = None
@@ -515,10 +536,13 @@ def main():
         threads = len(os.sched_getaffinity(0))
         frac = min(1.0, 8.0e6 / max(1, n_ints))
         rate, n_sample, reps, t_cpu = cpu_oracle_rate(hbs, frac, 10.0, threads)
+        rate1, n1, reps1, t1c = cpu_oracle_rate(hbs, frac / 8, 2.0, 1)
         cpu = {"value": rate, "unit": "ints/s", "cores": threads, "kind": "oracle",
                "sample": f"first {frac:.4f} of the lists of all {len(hbs)} batches "
                          f"({n_sample} ints), {reps} rep(s), {t_cpu:.1f} s, gco_decode_batch "
-                         "with the d-gap prefix sum"}
+                         "with the d-gap prefix sum",
+               "value_1_thread": rate1,
+               "sample_1_thread": f"first {frac / 8:.4f} of the lists ({n1} ints), {reps1} rep(s)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
@@ -538,7 +562,12 @@ def main():
                                 "serial: index then decode, variant by variant")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_decode (all variants)", "algorithmic_bytes_per_step": sum(algo)},
+                     "kernel": "k_decode (all variants)", "algorithmic_bytes_per_step": sum(algo),
+                     "frac_of_nominal_8tbs": achieved / 8000.0,
+                     "gaps_only": {"achieved": gaps_achieved, "frac": gaps_achieved / peak,
+                                   "path": "gc_decode (no d-gap scan), the paper's measured path"}},
+        "step_ms": {"mean": ms / args.steps, "median": step_ms[len(step_ms) // 2],
+                    "min": step_ms[0], "max": step_ms[-1]},
         "per_codec": per_codec,
         "cpu_baseline": cpu,
         "e2e": e2e,
