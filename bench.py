@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--encode", action="store_true",
                     help="time the GPU frame encoder (Group-PFD, SIMD-BP128) on config 3")
     ap.add_argument("--side-streams", type=int, default=1)
+    ap.add_argument("--strong", action="store_true",
+                    help="config 5: split the same workload over the ranks (strong scaling)")
     ap.add_argument("--sched", choices=["overlap", "serial"], default="overlap",
                     help="overlap: index stages on a side stream, concurrent with the decodes")
     ap.add_argument("--no-e2e", action="store_true")
@@ -77,7 +79,7 @@ def config_codecs(k: int, zeta):
 def make_workload(args, rank, world):
     """(workload, global id of its first list, scaling) of this rank (dist.shard_for_rank)."""
     from paper_1502_01916_b200 import dist
-    sh = dist.shard_for_rank(args.config, args.scale, rank, world)
+    sh = dist.shard_for_rank(args.config, args.scale, rank, world, strong=args.strong)
     return sh.workload, sh.list_base, sh.scaling
 
 

@@ -27,14 +27,21 @@ class Shard:
     scaling: str           # "weak" (replicas) or "strong" (one workload split by list)
 
 
-def shard_for_rank(config: int, scale: float, rank: int, world: int) -> Shard:
+def shard_for_rank(config: int, scale: float, rank: int, world: int, strong: bool = False) -> Shard:
     """The input of `rank`.  Config 5 is one 2^34-int workload defined across the 8 GPUs of
     a box: it is split by list at the sum(n) quantiles into 8 shards and rank
     r decodes shard r % 8, so per-GPU work is fixed and 8 ranks decode exactly config 5.
     Configs 1-4 give every rank its own independently drawn replica.  Both are weak
     scaling (per-GPU work fixed as the rank count grows)."""
     import gen
-    del world  # the split does not depend on the rank count (8 shards, SURVEY §8(e))
+    if config == 5 and strong:
+        # strong scaling (SURVEY §8(e), primary): the same workload split into `world`
+        # contiguous list ranges at the sum(n) quantiles, one per rank
+        w = gen.config(5, scale=scale, shard=rank, n_shards=world)
+        L = max(1, int(round(50_000_000 * scale)))
+        total = int(round((1 << 34) * scale))
+        ln = gen.zipf_lengths(L, total, 1.05, 1, 1 << 24, seed=4)
+        return Shard(w, int(gen.shard_bounds(ln, world)[rank]), "strong")
     if config == 5:
         n_shards, shard = 8, rank % 8
         w = gen.config(5, scale=scale, shard=shard, n_shards=n_shards)

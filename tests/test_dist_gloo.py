@@ -45,6 +45,21 @@ def test_config5_shards_partition_the_workload():
     assert [int(x) for x in got] == list(want)
 
 
+def test_config5_strong_split_covers_the_workload():
+    """Strong scaling: for every rank count the shards partition the same workload, and the
+    G7 checksum summed over the shards equals the whole workload's."""
+    full = gen.config(5, scale=SCALE5)
+    want = gen.checksum(full.list_n, full.values)
+    for world in (1, 2, 4, 8):
+        shards = [gdist.shard_for_rank(5, SCALE5, r, world, strong=True) for r in range(world)]
+        assert all(s.scaling == "strong" for s in shards)
+        assert np.array_equal(np.concatenate([s.workload.values for s in shards]), full.values)
+        got = np.zeros(3, np.uint64)
+        for s in shards:
+            got += np.array(gen.checksum(s.workload.list_n, s.workload.values, s.list_base), np.uint64)
+        assert [int(x) for x in got] == list(want)
+
+
 def test_replicas_are_independent_draws():
     a = gdist.shard_for_rank(2, 1 / 4096, 0, 2)
     b = gdist.shard_for_rank(2, 1 / 4096, 1, 2)
