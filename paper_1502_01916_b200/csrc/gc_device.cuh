@@ -47,7 +47,10 @@ constexpr uint32_t kR = kQPT * kThreads;         // quad ordinals per unpack rou
 #define GC_DCAP 1600
 #endif
 constexpr uint32_t kLC = GC_LC;                  // lists per list round (list table)
-constexpr uint32_t kUPT = 4;                     // parse units per thread per parse chunk
+#ifndef GC_UPT
+#define GC_UPT 4
+#endif
+constexpr uint32_t kUPT = GC_UPT;                // parse units per thread per parse chunk
 constexpr uint32_t kOutW = kT + 8;               // staging ints: index = tile position + 4
 constexpr uint32_t kCCap = GC_CCAP;              // staged control words
 constexpr uint32_t kDCap = GC_DCAP;              // staged data vectors (25 KiB)
