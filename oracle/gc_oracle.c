@@ -659,9 +659,51 @@ static int pfd_decode(uint32_t F, uint32_t n, const uint8_t* ctrl, uint64_t ctrl
 /* per-list dispatch                                                    */
 /* ------------------------------------------------------------------ */
 
+/* ------------------------------------------------------------------ */
+/* Variable Byte, §2.3: 7-bit groups, least significant */
+/* first; "the most significant bit of a byte is the continuation bit":  */
+/* MSB = 1 marks the LAST byte of an integer.  The byte stream is the     */
+/* control area; there is no data area.                                   */
+/* ------------------------------------------------------------------ */
+static int vb_encode(const uint32_t* x, uint32_t n, gco_stream* out) {
+  bytebuf cb = {0, 0, 0};
+  for (uint32_t i = 0; i < n; i++) {
+    uint32_t v = x[i];
+    while (v >= 128) {
+      if (bb_push(&cb, (uint8_t)(v & 127))) return GCO_ERR_NOMEM; /* continuation */
+      v >>= 7;
+    }
+    if (bb_push(&cb, (uint8_t)(v | 128))) return GCO_ERR_NOMEM;   /* last byte */
+  }
+  out->ctrl = cb.p ? cb.p : (uint8_t*)calloc(1, 1);
+  out->ctrl_bytes = cb.n;
+  out->nvec = 0;
+  out->data = (uint32_t*)calloc(4, 4);
+  return out->data ? GCO_OK : GCO_ERR_NOMEM;
+}
+
+static int vb_decode(uint32_t n, const uint8_t* ctrl, uint64_t ctrl_bytes, uint32_t* q) {
+  uint64_t p = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    uint64_t v = 0;
+    uint32_t k = 0;
+    for (;;) {
+      if (p >= ctrl_bytes) return GCO_ERR_TRUNCATED; /* stream ends mid-integer */
+      if (k == 5) return GCO_ERR_MALFORMED;          /* > 5 bytes without terminator */
+      uint8_t b = ctrl[p++];
+      v |= (uint64_t)(b & 127) << (7 * k);
+      k++;
+      if (b & 128) break;
+    }
+    q[i] = (uint32_t)v;
+  }
+  return GCO_OK;
+}
+
 static int check_params(const gco_params* p) {
   if (!p) return GCO_ERR_ARG;
   switch (p->codec) {
+    case GCO_VARBYTE:
     case GCO_GROUP_SIMPLE:
     case GCO_GROUP_AFOR:
       return GCO_OK;
@@ -681,6 +723,7 @@ int gco_encode_list(const gco_params* p, const uint32_t* x, uint32_t n, gco_stre
   if (rc) return rc;
   memset(out, 0, sizeof(*out));
   switch (p->codec) {
+    case GCO_VARBYTE: rc = vb_encode(x, n, out); break;
     case GCO_GROUP_SIMPLE: rc = gs_encode(x, n, out); break;
     case GCO_GROUP_SCHEME: rc = gsc_encode(p->variant, x, n, out); break;
     case GCO_GROUP_AFOR: rc = afor_encode(x, n, out); break;
@@ -699,6 +742,7 @@ int gco_decode_list(const gco_params* p, uint32_t n, const uint8_t* ctrl, uint64
   uint32_t* q = (uint32_t*)calloc((size_t)(4 * (Q ? Q : 1)), 4);
   if (!q) return GCO_ERR_NOMEM;
   switch (p->codec) {
+    case GCO_VARBYTE: rc = vb_decode(n, ctrl, ctrl_bytes, q); break;
     case GCO_GROUP_SIMPLE: rc = gs_decode(n, ctrl, ctrl_bytes, data, nvec, q); break;
     case GCO_GROUP_SCHEME: rc = gsc_decode(p->variant, n, ctrl, ctrl_bytes, data, nvec, q); break;
     case GCO_GROUP_AFOR: rc = afor_decode(n, ctrl, ctrl_bytes, data, nvec, q); break;

@@ -22,6 +22,7 @@ extern "C" {
 #endif
 
 /* Codec ids. */
+#define GCO_VARBYTE 1
 #define GCO_GROUP_SIMPLE 2
 #define GCO_GROUP_SCHEME 3
 #define GCO_GROUP_AFOR 4

@@ -16,7 +16,7 @@ SRC = os.path.join(HERE, "gc_oracle.c")
 HDR = os.path.join(HERE, "gc_oracle.h")
 LIB = os.path.join(HERE, "liboracle.so")
 
-GROUP_SIMPLE, GROUP_SCHEME, GROUP_AFOR, GROUP_PFD = 2, 3, 4, 5
+VARBYTE, GROUP_SIMPLE, GROUP_SCHEME, GROUP_AFOR, GROUP_PFD = 1, 2, 3, 4, 5
 ERRORS = {0: "ok", 1: "arg", 2: "malformed", 3: "truncated", 4: "bad_magic", 5: "version",
           6: "codec", 7: "variant", 8: "nomem", 9: "not_increasing"}
 

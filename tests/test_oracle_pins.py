@@ -450,3 +450,39 @@ def test_bp128_frames_at_max_width_no_exceptions(F):
             vec += (q * b + 31) // 32
         assert int(bt["data_off"][1]) == vec
         assert np.array_equal(O.decode_batch(bt, dgaps=False), x)
+
+
+def test_varbyte_spec_bytes_and_errors():
+    """Variable Byte (P §2.3): 7-bit groups least significant first, MSB = 1
+    on the LAST byte.  SPEC's derived bytes, its two errors, and the length rule
+    ceil(width/7) (width(0) = 1) at every 7-bit boundary."""
+    def enc(x):
+        return [int(b) for b in O.encode_list(np.array(x, np.uint32), O.VARBYTE)["ctrl"]]
+    assert enc([5]) == [0x85]
+    assert enc([300]) == [0x2C, 0x82]
+    assert enc([0]) == [0x80]
+    assert enc([5, 300, 0]) == [0x85, 0x2C, 0x82, 0x80]
+    with pytest.raises(O.OracleError):  # stream ends mid-integer
+        O.decode_list(1, np.array([0x2C], np.uint8), np.zeros((0, 4), np.uint32), codec=O.VARBYTE)
+    with pytest.raises(O.OracleError):  # more than 5 bytes without a terminator
+        O.decode_list(1, np.zeros(6, np.uint8), np.zeros((0, 4), np.uint32), codec=O.VARBYTE)
+    for k in range(0, 5):
+        for v in {(1 << (7 * k)) - 1, 1 << (7 * k), min((1 << (7 * k + 7)) - 1, 2**32 - 1)}:
+            if v < 0 or v >= 2**32:
+                continue
+            w = max(1, int(v).bit_length())
+            assert len(enc([v])) == -(-w // 7), v
+    assert len(enc([2**32 - 1])) == 5
+
+
+def test_varbyte_round_trip():
+    rng = np.random.default_rng(77)
+    for n, bits in ((0, 1), (1, 32), (63, 7), (64, 8), (1000, 21), (500, 32)):
+        x = rng.integers(0, 1 << bits, n, dtype=np.uint64).astype(np.uint32)
+        e = O.encode_list(x, O.VARBYTE)
+        assert np.array_equal(O.decode_list(n, e["ctrl"], e["data"], codec=O.VARBYTE), x)
+    ln = rng.integers(0, 64, 200).astype(np.uint32)
+    docs = np.concatenate([np.cumsum(rng.integers(1, 1000, int(k))).astype(np.uint32) for k in ln])
+    bt = O.encode_batch(docs, ln, O.VARBYTE, delta=True)
+    assert bt["data"].shape[0] == 0
+    assert np.array_equal(O.decode_batch(bt, dgaps=True), docs)
