@@ -57,7 +57,12 @@ typedef enum {
 } gc_status;
 
 /* Codec ids. */
-typedef enum { GC_GROUP_SIMPLE = 2, GC_GROUP_SCHEME = 3, GC_GROUP_AFOR = 4, GC_GROUP_PFD = 5 } gc_codec;
+/* GC_VARBYTE (P §2.3): the short-list fallback of P:L640 §7.5; its byte
+ * stream (7-bit groups, least significant first, MSB = 1 on an int's last byte) is the
+ * control area (ctrl / ctrl_off, byte offsets), there is no data area (data_off all 0);
+ * decode and encode as the other codecs (no GPU encoder). */
+typedef enum { GC_VARBYTE = 1, GC_GROUP_SIMPLE = 2, GC_GROUP_SCHEME = 3, GC_GROUP_AFOR = 4,
+               GC_GROUP_PFD = 5 } gc_codec;
 
 /* Sticky device status bits, OR-ed by the kernels into the workspace. */
 enum {

@@ -87,6 +87,19 @@ class ListEncoder {
   }
 
   void encode(const uint32_t* x, uint32_t n, Buf& b) {
+    if (p_.codec == GC_VARBYTE) {  // P §2.3: 7-bit groups, least significant first, MSB=1 last
+      const size_t c0 = b.ctrl.size();
+      for (uint32_t i = 0; i < n; i++) {
+        uint32_t v = x[i];
+        while (v >= 128) {
+          b.ctrl.push_back((uint8_t)(v & 127));
+          v >>= 7;
+        }
+        b.ctrl.push_back((uint8_t)(v | 128));
+      }
+      pad_ctrl(b, c0);
+      return;
+    }
     const uint64_t Q = cdiv(n, 4);
     quads_.assign(4 * Q, 0);
     std::memcpy(quads_.data(), x, 4ull * n);
@@ -322,6 +335,7 @@ void run_job(const gc_encode_params& p, const uint32_t* values, const uint32_t* 
 bool valid_params(const gc_encode_params* p) {
   if (!p) return false;
   switch (p->codec) {
+    case GC_VARBYTE:
     case GC_GROUP_SIMPLE:
     case GC_GROUP_AFOR:
       return true;

@@ -494,6 +494,82 @@ using namespace gcd;
 
 namespace {
 
+// ------------------------------------------------------------------ Variable Byte
+// The short-list fallback (§7.5; P §2.3): one warp per list reads its bytes 32 at a
+// time; a ballot of the last-byte bits (MSB = 1) ranks the ints, each last byte assembles
+// its int from the (<= 4) bytes before it -- shuffles, and the previous round's last four
+// bytes -- and a warp scan gives the d-gap prefix sum.  Bytes after the list's n ints
+// (the 4-byte padding of the list's area) are ignored.
+template <bool DGAPS>
+__global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(D.ctrl_words);
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t err = 0;
+  for (uint64_t l = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < D.n_lists;
+       l += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t n = D.list_n[l];
+    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
+    if (c1 < c0 || c1 > 4 * D.n_ctrl_words) {
+      if (n) err |= GC_DEV_TRUNCATED;
+      continue;
+    }
+    uint32_t got = 0, run = 0, carry = 0;  // ints so far, bytes of the open int, d-gap carry
+    uint32_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;  // the previous round's last four bytes
+    for (uint64_t r = c0; r < c1 && got < n; r += 32) {
+      const uint64_t p = r + lane;
+      const uint32_t b = p < c1 ? bytes[p] : 0u;
+      const uint32_t stops = __ballot_sync(0xffffffffu, p < c1 && (b & 128u));
+      const uint32_t before = stops & lt;
+      // bytes of my int before me: since the last stop before me (this round), or the run
+      // carried in from earlier rounds
+      const uint32_t k = before ? lane - (31u - __clz(before)) - 1u : lane + run;
+      const uint32_t s1 = __shfl_up_sync(0xffffffffu, b, 1), s2 = __shfl_up_sync(0xffffffffu, b, 2);
+      const uint32_t s3 = __shfl_up_sync(0xffffffffu, b, 3), s4 = __shfl_up_sync(0xffffffffu, b, 4);
+      const uint32_t prev[5] = {b, lane >= 1 ? s1 : p1, lane >= 2 ? s2 : (lane == 1 ? p1 : p2),
+                                lane >= 3 ? s3 : (lane == 2 ? p1 : (lane == 1 ? p2 : p3)),
+                                lane >= 4 ? s4 : (lane == 3 ? p1 : (lane == 2 ? p2 : (lane == 1 ? p3 : p4)))};
+      uint32_t v = 0;
+      const bool mine = (stops >> lane) & 1u;
+      const uint32_t idx = got + __popc(before);
+      if (mine) {
+        if (k > 4) err |= GC_DEV_BAD_LD;  // more than 5 bytes without a terminator
+        for (uint32_t j = 0; j <= min(k, 4u); j++) v |= (prev[j] & 127u) << (7 * (min(k, 4u) - j));
+      }
+      const bool keep = mine && idx < n;
+      uint32_t inc = keep ? v : 0u;
+      if (DGAPS) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= (uint32_t)o) inc += t;
+        }
+      }
+      if (keep) out[o0 + idx] = DGAPS ? carry + inc : v;
+      if (DGAPS) carry += __shfl_sync(0xffffffffu, inc, 31);
+      got += __popc(stops);
+      const uint32_t last = stops ? 31u - __clz(stops) : 0u;
+      run = stops ? 31u - last : run + 32u;  // bytes after the round's last stop
+      p4 = __shfl_sync(0xffffffffu, b, 28);
+      p3 = __shfl_sync(0xffffffffu, b, 29);
+      p2 = __shfl_sync(0xffffffffu, b, 30);
+      p1 = __shfl_sync(0xffffffffu, b, 31);
+    }
+    if (got < n) err |= GC_DEV_TRUNCATED;  // the stream ends before n ints
+  }
+  err = __reduce_or_sync(0xffffffffu, err);
+  if (lane == 0 && err) atomicOr(&D.hdr->status, err);
+}
+
+int num_sms();
+gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
+  if (!(stages & GC_STAGE_DECODE)) return GC_OK;
+  const uint64_t blocks = mn64((D.n_lists + 7) / 8, (uint64_t)num_sms() * 16);
+  if (dgaps) k_varbyte<true><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+  else k_varbyte<false><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
 struct WsLayout {
   uint64_t n_tiles_a, n_tiles_b;
   uint64_t off_tiles_a, off_tiles_b, off_entries, off_first, bytes;
@@ -517,6 +593,7 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 gc_status check_codec(const gc_batch* b) {
   switch (b->codec) {
+    case GC_VARBYTE:
     case GC_GROUP_SIMPLE:
     case GC_GROUP_AFOR:
       return b->variant == 0 ? GC_OK : GC_ERR_BAD_VARIANT;
@@ -651,6 +728,8 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.entries = (Entry*)(w + L.off_entries);
   D.first_list = (uint32_t*)(w + L.off_first);
   switch (b->codec) {
+    case GC_VARBYTE:
+      return launch_varbyte(D, out, dgaps, st, stages);
     case GC_GROUP_SIMPLE:
       return launch_codec<CodecGS>(D, out, dgaps, st, stages);
     case GC_GROUP_AFOR:

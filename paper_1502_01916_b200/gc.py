@@ -15,7 +15,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GC_LIB") or os.path.join(_PKG, "libgc.so")
 
-GROUP_SIMPLE, GROUP_SCHEME, GROUP_AFOR, GROUP_PFD = 2, 3, 4, 5
+VARBYTE, GROUP_SIMPLE, GROUP_SCHEME, GROUP_AFOR, GROUP_PFD = 1, 2, 3, 4, 5
 CODEC_NAMES = {GROUP_SIMPLE: "group_simple", GROUP_SCHEME: "group_scheme",
                GROUP_AFOR: "group_afor", GROUP_PFD: "group_pfd"}
 DEV_BITS = {1: "BAD_SELECTOR", 2: "BAD_LD", 4: "BAD_FRAME", 8: "BAD_EXCEPTION", 16: "TRUNCATED"}
@@ -101,7 +101,7 @@ def codec_label(codec: int, variant: int = 0, frame_quads: int = 32) -> str:
     if codec == GROUP_PFD:
         name = "BP128" if variant == 1 else "G-PFD"
         return name if frame_quads == 32 else f"{name}-F{frame_quads}"
-    return {GROUP_SIMPLE: "G-SIM", GROUP_AFOR: "G-AFOR"}[codec]
+    return {VARBYTE: "VByte", GROUP_SIMPLE: "G-SIM", GROUP_AFOR: "G-AFOR"}[codec]
 
 
 # ----------------------------------------------------------------------------- batches

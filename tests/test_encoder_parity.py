@@ -13,7 +13,7 @@ import oracle as O
 from paper_1502_01916_b200 import gc
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CODECS = ([(O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
+CODECS = ([(O.VARBYTE, 0), (O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
                                    for cg, k in gc.GSC_VARIANTS]
           + [(O.GROUP_AFOR, 0), (O.GROUP_PFD, 0), (O.GROUP_PFD, 1)])
 

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1502_01916_b200 import gc  # noqa: E402
 
-CODECS = ([(O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
+CODECS = ([(O.VARBYTE, 0), (O.GROUP_SIMPLE, 0)] + [(O.GROUP_SCHEME, O.gsc_variant(cg, k))
                                    for cg, k in gc.GSC_VARIANTS]
           + [(O.GROUP_AFOR, 0), (O.GROUP_PFD, 0), (O.GROUP_PFD, 1)])
 IDS = [gc.codec_label(c, v) for c, v in CODECS]
@@ -128,6 +128,16 @@ def test_malformed_streams_flagged_not_faulting():
     hb.ctrl[:8] = 0xFF                                        # runs of 32+ ones
     _, s = gpu_decode(hb, True)
     assert s & 2
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.VARBYTE))
+    hb.ctrl = hb.ctrl.copy()
+    hb.ctrl[:] = 0                                           # no int ever terminates
+    _, s = gpu_decode(hb, True)
+    assert s & (2 | 16)                                      # > 5 bytes / truncated
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.VARBYTE))
+    hb.ctrl_off = hb.ctrl_off.copy()
+    hb.ctrl_off[1:] = np.minimum(hb.ctrl_off[1:], hb.ctrl_off[1])  # lists 1.. have no bytes
+    _, s = gpu_decode(hb, True)
+    assert s & 16
     hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_PFD, 0))
     if hb.exc_off[-1] > 0:                                   # a PFD frame with exceptions
         hb.variant = 1                                       # read as BP128: none allowed
