@@ -261,6 +261,57 @@ def encode_device(values, list_n, codec: int = GROUP_PFD, variant: int = 0, delt
                        int(sizes[2]))
 
 
+# ----------------------------------------------------------------------------- posting store
+@dataclasses.dataclass
+class PostingStore:
+    """P:L640 §7.5's rule: lists shorter than `threshold` (64) are Variable Byte encoded
+    whatever the codec of the others.  The lists keep their order within
+    each group; the decoded output holds the long group first and the short group from the
+    16-byte aligned offset `short_base`; `list_out_off[i]` locates original list i in it."""
+    long: HostBatch
+    short: HostBatch
+    list_out_off: np.ndarray   # uint64 [L]
+    short_base: int
+    total: int                 # ints of the decoded output (incl. the alignment gap)
+
+
+def encode_posting_store(values: np.ndarray, list_n: np.ndarray, codec: int, variant: int = 0,
+                         delta: bool = False, threshold: int = 64, **kw) -> PostingStore:
+    v = np.ascontiguousarray(values, np.uint32)
+    ln = np.ascontiguousarray(list_n, np.uint32)
+    starts = np.concatenate([[0], np.cumsum(ln.astype(np.int64))[:-1]]) if len(ln) else np.zeros(0, np.int64)
+    is_short = ln < threshold
+    idx = {True: np.nonzero(is_short)[0], False: np.nonzero(~is_short)[0]}
+
+    def gather(ids):
+        if len(ids) == 0:
+            return np.zeros(0, np.uint32)
+        return np.concatenate([v[starts[i]:starts[i] + ln[i]] for i in ids])
+    longb = encode_batch(gather(idx[False]), ln[idx[False]], codec, variant, delta=delta, **kw)
+    shortb = encode_batch(gather(idx[True]), ln[idx[True]], VARBYTE, 0, delta=delta)
+    short_base = (longb.total_out + 3) & ~3
+    off = np.zeros(len(ln), np.uint64)
+    off[idx[False]] = longb.out_off[:-1]
+    off[idx[True]] = short_base + shortb.out_off[:-1]
+    return PostingStore(longb, shortb, off, short_base, short_base + shortb.total_out)
+
+
+def decode_posting_store(store: PostingStore, dgaps: bool = True, device="cuda", stream=None):
+    """Both groups decoded into one output (int32 view of uint32): the long group with its
+    codec, the short group with Variable Byte.  Returns (out, (ws_long, ws_short))."""
+    import torch
+    out = torch.empty(max(store.total, 4), dtype=torch.int32, device=device)
+    fn = decode_dgaps if dgaps else decode
+    wss = []
+    for hb, base in ((store.long, 0), (store.short, store.short_base)):
+        db = to_device(hb, device)
+        ws = alloc_workspace(db, device)
+        fn(db, out=out[base:base + max(hb.total_out, 4)] if hb.total_out else out, ws=ws,
+           stream=stream)
+        wss.append(ws)
+    return out[:store.total], tuple(wss)
+
+
 def to_device(hb: HostBatch, device="cuda", pin: bool = False) -> DeviceBatch:
     import torch
 

@@ -71,3 +71,21 @@ def test_encoder_rejects_bad_input():
                         variant=gc.gsc_variant(1, "B") | (2 << 2))
     with pytest.raises(gc.GcError):
         gc.encode_batch(np.array([1], np.uint32), np.array([1], np.uint32), 9)
+
+
+def test_posting_store_short_lists_are_varbyte():
+    """P:L640 §7.5: lists shorter than 64 are Variable Byte encoded whatever
+    the requested codec; every original list is found at list_out_off (checked by decoding
+    both groups with the oracle)."""
+    w = gen.config(5, scale=2 ** -17)  # Zipf(1.05) over [1, 2^24]: most lists are short
+    st = gc.encode_posting_store(w.values, w.list_n, O.GROUP_SCHEME, O.gsc_variant(1, "CU"),
+                                 delta=True)
+    assert st.short.codec == O.VARBYTE and np.all(st.short.list_n < 64)
+    assert np.all(st.long.list_n >= 64) and len(st.short.list_n) + len(st.long.list_n) == len(w.list_n)
+    out = np.zeros(st.total, np.uint32)
+    out[:st.long.total_out] = O.decode_batch(st.long.as_dict(), dgaps=True)
+    out[st.short_base:] = O.decode_batch(st.short.as_dict(), dgaps=True)
+    starts = np.concatenate([[0], np.cumsum(w.list_n.astype(np.int64))[:-1]])
+    for i in range(len(w.list_n)):
+        o, n = int(st.list_out_off[i]), int(w.list_n[i])
+        assert np.array_equal(out[o:o + n], w.values[starts[i]:starts[i] + n]), i

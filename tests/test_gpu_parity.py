@@ -242,3 +242,20 @@ def test_fuzz_repeated(codec, variant):
             got = out[:hb.total_out].cpu().numpy().view(np.uint32)
             bad = np.nonzero(got != want)[0]
             assert len(bad) == 0, f"trial {trial} rep {rep}: {len(bad)} mismatches, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("codec,variant", [(O.GROUP_SIMPLE, 0), (O.GROUP_SCHEME, O.gsc_variant(8, "IU")),
+                                           (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0)])
+def test_posting_store(codec, variant):
+    """The §7.5 posting store on config 5's shape (72% of lists shorter than 64): long lists
+    with the codec, short ones with Variable Byte, one output, every list at its offset."""
+    w = gen.config(5, scale=2 ** -14)
+    st = gc.encode_posting_store(w.values, w.list_n, codec, variant, delta=True)
+    out, wss = gc.decode_posting_store(st, dgaps=True)
+    torch.cuda.synchronize()
+    assert all(gc.read_device_status(ws) == 0 for ws in wss)
+    got = out.cpu().numpy().view(np.uint32)
+    starts = np.concatenate([[0], np.cumsum(w.list_n.astype(np.int64))[:-1]])
+    for i in range(len(w.list_n)):
+        o, n = int(st.list_out_off[i]), int(w.list_n[i])
+        assert np.array_equal(got[o:o + n], w.values[starts[i]:starts[i] + n]), i
