@@ -71,9 +71,11 @@ def config_codecs(k: int, zeta):
         return [(gc.GROUP_PFD, 0, 32, zeta), (gc.GROUP_PFD, 1, 32, zeta)]
     if k == 4:
         return [(gc.GROUP_AFOR, 0, 32, zeta)]
+    # config 5: all four Group codecs (GSC's two representatives) + Variable Byte, the
+    # paper's baseline / short-list fallback (P §2.3)
     return [(gc.GROUP_SIMPLE, 0, 32, zeta), (gc.GROUP_SCHEME, gc.gsc_variant(1, "CU"), 32, zeta),
             (gc.GROUP_SCHEME, gc.gsc_variant(8, "IU"), 32, zeta), (gc.GROUP_AFOR, 0, 32, zeta),
-            (gc.GROUP_PFD, 0, 32, zeta)]
+            (gc.GROUP_PFD, 0, 32, zeta), (gc.VARBYTE, 0, 32, zeta)]
 
 
 def make_workload(args, rank, world):
@@ -325,10 +327,22 @@ def main():
     # ---- inputs (untimed): generate, encode with the library's host encoder, copy to HBM
     t_setup = time.perf_counter()
     w, list_base, scaling = make_workload(args, rank, world)
-    hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
-           for c, v, f, z in codecs]
+
+    def subset(c):  # Variable Byte is the short-list fallback (§7.5): lists < 64
+        if c != gc.VARBYTE:
+            return w.values, w.list_n
+        ln = w.list_n.astype(np.int64)
+        st = np.concatenate([[0], np.cumsum(ln)[:-1]])
+        ids = np.nonzero(w.list_n < 64)[0]
+        vals = (np.concatenate([w.values[st[i]:st[i] + ln[i]] for i in ids]) if len(ids)
+                else np.zeros(0, np.uint32))
+        return vals, w.list_n[ids]
+    subs = [subset(c) for c, _, _, _ in codecs]
+    hbs = [gc.encode_batch(sv, sl, c, v, delta=w.delta, frame_quads=f, zeta=z)
+           for (sv, sl), (c, v, f, z) in zip(subs, codecs)]
     dbs = [gc.to_device(hb, dev) for hb in hbs]
-    n_ints = w.n_ints
+    n_ints = max(hb.total_out for hb in hbs)          # (the largest batch)
+    n_ints_all = sum(hb.total_out for hb in hbs)      # ints decoded per step
     out = torch.empty(max(n_ints, 4), dtype=torch.int32, device=dev)
     wss = [gc.alloc_workspace(db, dev) for db in dbs]
     stream = torch.cuda.current_stream(dev)
@@ -337,12 +351,12 @@ def main():
     # ---- parity gate (untimed): every variant bit-exact against the generator
     verified = None
     if not args.no_verify:
-        vals = torch.from_numpy(w.values.view(np.int32)).to(dev)
-        ln = torch.from_numpy(w.list_n.astype(np.int64)).to(dev)
-        starts = torch.cumsum(ln, 0) - ln
-        starts = starts[ln > 0]
         verified = True
-        for lab, db, ws in zip(labels, dbs, wss):
+        for lab, db, ws, (sv, sl) in zip(labels, dbs, wss, subs):
+            vals = torch.from_numpy(np.ascontiguousarray(sv).view(np.int32)).to(dev)
+            ln = torch.from_numpy(sl.astype(np.int64)).to(dev)
+            starts = torch.cumsum(ln, 0) - ln
+            starts = starts[ln > 0]
             gaps, _ = gc.decode(db, out=out, ws=ws)
             ok_g = bool(torch.equal(gaps, vals)) if not w.delta else None
             docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
@@ -491,7 +505,7 @@ def main():
         chk += gc.checksum(db, docs, list_base=list_base).cpu().numpy().view(np.uint64)
     from paper_1502_01916_b200 import dist as gdist
     ms, total_ints, _, all_verified, chk = gdist.reduce_run(
-        pg, dev, ms, int(n_ints) * len(dbs), status, verified, chk)
+        pg, dev, ms, int(n_ints_all), status, verified, chk)
     if rank != 0:
         if pg:
             pg.destroy_process_group()
@@ -567,8 +581,8 @@ def main():
         torch.cuda.synchronize(dev)
         ems = a0.elapsed_time(a1)
         h2d = sum(p.directory_bytes + len(p.ctrl) + 16 * len(p.data) + len(p.exc) for p, _ in pinned)
-        e2e = {"value": n_ints * len(pinned) * args.e2e_steps / (ems / 1e3), "unit": "ints/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * n_ints * len(pinned)),
+        e2e = {"value": n_ints_all * args.e2e_steps / (ems / 1e3), "unit": "ints/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * n_ints_all),
                "steps": args.e2e_steps, "ms_per_step": ems / args.e2e_steps,
                "api": "gc_decode_host (pinned host buffers, batches alternating over 2 streams)"}
 
@@ -592,7 +606,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": w.name, "n_ints_per_gpu": n_ints, "n_lists_per_gpu": int(len(w.list_n)),
+        "config": {"workload": w.name, "n_ints_per_gpu": w.n_ints, "n_lists_per_gpu": int(len(w.list_n)),
                    "codecs": labels, "ints_per_step_all_gpus": ints_per_step_all,
                    "parallelism": f"dp{world} (lists sharded by rank, {scaling} scaling)",
                    "l2": (f"flushed before every timed step (scratch write of {4 * l2_bytes >> 20} MB; "

@@ -48,7 +48,8 @@ def codecs_of(k: int):
     if k == 4:
         return [(O.GROUP_AFOR, 0)]
     return [(O.GROUP_SIMPLE, 0), (O.GROUP_SCHEME, O.gsc_variant(1, "CU")),
-            (O.GROUP_SCHEME, O.gsc_variant(8, "IU")), (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0)]
+            (O.GROUP_SCHEME, O.gsc_variant(8, "IU")), (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0),
+            (O.VARBYTE, 0)]
 
 
 def run_config(w, codecs, list_base=0):
