@@ -500,6 +500,45 @@ namespace {
 // its int from the (<= 4) bytes before it -- shuffles, and the previous round's last four
 // bytes -- and a warp scan gives the d-gap prefix sum.  Bytes after the list's n ints
 // (the 4-byte padding of the list's area) are ignored.
+// Short lists (n < kVbShort, the fallback's case): one thread per list, a serial byte loop.
+constexpr uint32_t kVbShort = 64;
+template <bool DGAPS>
+__global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restrict__ out) {
+  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(D.ctrl_words);
+  uint32_t err = 0;
+  for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < D.n_lists;
+       l += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = D.list_n[l];
+    if (n == 0 || n >= kVbShort) continue;
+    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
+    if (c1 < c0 || c1 > 4 * D.n_ctrl_words) {
+      err |= GC_DEV_TRUNCATED;
+      continue;
+    }
+    uint64_t p = c0;
+    uint32_t acc = 0;
+    for (uint32_t i = 0; i < n; i++) {
+      uint32_t v = 0, k = 0;
+      for (;;) {
+        if (p >= c1) {
+          err |= GC_DEV_TRUNCATED;
+          break;
+        }
+        if (k == 5) {
+          err |= GC_DEV_BAD_LD;
+          break;
+        }
+        const uint32_t b = bytes[p++];
+        v |= (b & 127u) << (7 * k);
+        k++;
+        if (b & 128u) break;
+      }
+      acc = DGAPS ? acc + v : v;
+      out[o0 + i] = acc;
+    }
+  }
+  if (err) atomicOr(&D.hdr->status, err);
+}
 template <bool DGAPS>
 __global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ out) {
   const uint32_t lane = threadIdx.x & 31;
@@ -509,9 +548,10 @@ __global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ o
   for (uint64_t l = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < D.n_lists;
        l += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
     const uint32_t n = D.list_n[l];
+    if (n < kVbShort) continue;  // (k_varbyte_short)
     const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
     if (c1 < c0 || c1 > 4 * D.n_ctrl_words) {
-      if (n) err |= GC_DEV_TRUNCATED;
+      err |= GC_DEV_TRUNCATED;
       continue;
     }
     uint32_t got = 0, run = 0, carry = 0;  // ints so far, bytes of the open int, d-gap carry
@@ -565,8 +605,14 @@ int num_sms();
 gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
   if (!(stages & GC_STAGE_DECODE)) return GC_OK;
   const uint64_t blocks = mn64((D.n_lists + 7) / 8, (uint64_t)num_sms() * 16);
-  if (dgaps) k_varbyte<true><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
-  else k_varbyte<false><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+  const uint64_t sblocks = mn64((D.n_lists + 255) / 256, (uint64_t)num_sms() * 16);
+  if (dgaps) {
+    k_varbyte_short<true><<<(unsigned)mx64(sblocks, 1), 256, 0, st>>>(D, out);
+    k_varbyte<true><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+  } else {
+    k_varbyte_short<false><<<(unsigned)mx64(sblocks, 1), 256, 0, st>>>(D, out);
+    k_varbyte<false><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+  }
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
 
