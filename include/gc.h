@@ -159,6 +159,17 @@ enum { GC_STAGE_RESET = 1, GC_STAGE_INDEX = 2, GC_STAGE_DECODE = 4, GC_STAGE_ALL
 gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream, int dgaps, int stage_mask);
 
+/* Random access (the skip pointers of P:L640 at the decoder's tile
+ * granularity): decode the output ints [first, first + count) -- in whole tiles of
+ * 8192 ints, so every int of the tiles covering the range is written to its usual place
+ * in `out` (the full-size output buffer) and nothing else is.  `ws` must hold a complete
+ * gc_decode (dgaps == 0) / gc_decode_dgaps (dgaps != 0) of the same batch: its per-tile
+ * entries (control word, quad / data / exception prefixes) are the skip table and its
+ * per-tile inclusive d-gap prefixes the carries, so neither the reset nor the index stage
+ * runs.  Not for GC_VARBYTE (GC_ERR_UNKNOWN_CODEC).  Asynchronous on `stream`. */
+gc_status gc_decode_range(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          uint64_t first, uint64_t count, int dgaps, void* stream);
+
 /* Copy the sticky GC_DEV_* bits of a workspace to *host_bits.  Synchronises
  * `stream`.  0 means the last decode on this workspace saw a well-formed batch. */
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream);

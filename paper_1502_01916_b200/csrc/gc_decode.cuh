@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   // Entries of `tile` -> s_e (one warp)
   auto load_entries = [&](uint32_t tile) {
-    if (tile < D.n_tiles_b) {
+    if (tile < D.tile_end) {
       if (lane < 16) {
         reinterpret_cast<uint32_t*>(s_e)[lane] =
             reinterpret_cast<const uint32_t*>(D.entries + tile)[lane];
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     const bool last = tile + 1 == D.n_tiles_b;
     g.ok = 0;
     uint32_t cbytes = 0, xbytes = 0, dbytes = 0;
-    if (tile < D.n_tiles_b) {
+    if (tile < D.tile_end) {
       const uint64_t wa = E0.w, wb = last ? cend - 1 : E1.w;
       g.ok = (E0.valid && (last || E1.valid) && wb >= wa && wb < D.n_ctrl_words &&
               E0.l < D.n_lists && (last || (E1.l >= E0.l && E1.l < D.n_lists))) ? 1u : 0u;
@@ -254,19 +254,20 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
   }
-  if (warp == 0) load_entries(blockIdx.x);
+  const uint32_t first_tile = D.tile_begin + blockIdx.x;
+  if (warp == 0) load_entries(first_tile);
   if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kDT words
   if (tid == 0) {
     s_reset0[0] = kT;
     s_pend.on = 0;
   }
   __syncthreads();
-  if (tid == 0) setup(blockIdx.x, 0);
+  if (tid == 0) setup(first_tile, 0);
   __syncthreads();
 
   uint32_t buf = 0;
   long long t_last = clock64();
-  for (uint32_t tile = blockIdx.x; tile < D.n_tiles_b; tile += gridDim.x, buf ^= 1u) {
+  for (uint32_t tile = first_tile; tile < D.tile_end; tile += gridDim.x, buf ^= 1u) {
     GC_T(0);
     // warp 1 prefetches the next tile's entries (read after this tile's unpack)
     if (warp == 1) load_entries(tile + gridDim.x);

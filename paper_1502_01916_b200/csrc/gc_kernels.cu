@@ -48,6 +48,7 @@ struct Dev {
   uint64_t* tiles_b;
   Entry* entries;
   uint32_t* first_list;   // [n_tiles_a] 1 + owner list of the first word of control tile a
+  uint32_t tile_begin, tile_end;  // k_decode: the output tiles to decode (gc_decode_range)
 };
 
 // Per-list view used by the group walks of the index kernel.
@@ -728,7 +729,8 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   }
   // tiles are assigned round-robin to a co-resident grid (the decoupled look-back waits on
   // earlier tiles, which must all be running): a cooperative launch guarantees residency
-  const unsigned grid = (unsigned)mn64(D.n_tiles_b, (uint64_t)num_sms() * per_sm[dgaps]);
+  const unsigned grid = (unsigned)mn64(D.tile_end - D.tile_begin, (uint64_t)num_sms() * per_sm[dgaps]);
+  if (grid == 0) return GC_OK;
   Dev Dv = D;
   void* args[] = {&Dv, &out};
   if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kDT), args, smem, st) !=
@@ -738,7 +740,8 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
 }
 
 gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
-                      void* stream, bool dgaps, int stages = GC_STAGE_ALL) {
+                      void* stream, bool dgaps, int stages = GC_STAGE_ALL,
+                      uint64_t range_first = 0, uint64_t range_count = ~0ull) {
   gc_status s = check_batch(b, true);
   if (s != GC_OK) return s;
   if (!ws || !aligned16(ws) || (b->total_out && (!out || !aligned16(out))))
@@ -773,6 +776,9 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
   D.entries = (Entry*)(w + L.off_entries);
   D.first_list = (uint32_t*)(w + L.off_first);
+  D.tile_begin = (uint32_t)mn64(range_first / kT, L.n_tiles_b);
+  D.tile_end = (uint32_t)(range_count == ~0ull ? L.n_tiles_b
+                                               : mn64((range_first + range_count + kT - 1) / kT, L.n_tiles_b));
   switch (b->codec) {
     case GC_VARBYTE:
       return launch_varbyte(D, out, dgaps, st, stages);
@@ -844,6 +850,14 @@ gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t w
                           void* stream, int dgaps, int stage_mask) {
   if (stage_mask & ~GC_STAGE_ALL) return GC_ERR_INVALID_ARGUMENT;
   return decode_impl(b, out, ws, ws_bytes, stream, dgaps != 0, stage_mask);
+}
+
+gc_status gc_decode_range(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
+                          uint64_t first, uint64_t count, int dgaps, void* stream) {
+  if (b && b->codec == GC_VARBYTE) return GC_ERR_UNKNOWN_CODEC;  // (no tiles)
+  if (!b || first > b->total_out || count > b->total_out - first) return GC_ERR_INVALID_ARGUMENT;
+  if (count == 0) return GC_OK;
+  return decode_impl(b, out, ws, ws_bytes, stream, dgaps != 0, GC_STAGE_DECODE, first, count);
 }
 
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream) {

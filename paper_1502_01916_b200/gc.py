@@ -60,6 +60,7 @@ def _lib():
             "gc_decode": (i32, [P(CBatch), vp, vp, u64, vp]),
             "gc_decode_dgaps": (i32, [P(CBatch), vp, vp, u64, vp]),
             "gc_decode_stage": (i32, [P(CBatch), vp, vp, u64, vp, i32, i32]),
+            "gc_decode_range": (i32, [P(CBatch), vp, vp, u64, u64, u64, i32, vp]),
             "gc_read_device_status": (i32, [vp, P(C.c_uint32), vp]),
             "gc_checksum": (i32, [P(CBatch), vp, u64, vp, vp]),
             "gc_host_scratch_size": (i32, [P(CBatch), P(u64)]),
@@ -374,6 +375,17 @@ def decode_dgaps(batch: DeviceBatch, out=None, ws=None, stream=None):
 
 
 STAGE_RESET, STAGE_INDEX, STAGE_DECODE, STAGE_ALL = 1, 2, 4, 7
+
+
+def decode_range(batch: DeviceBatch, out, ws, first: int, count: int, dgaps: bool = True,
+                 stream=None):
+    """gc_decode_range: random access -- the tiles covering output ints [first, first+count)
+    decoded into the full-size `out`, from the skip table a complete decode left in `ws`."""
+    b = batch.cstruct()
+    st = _lib().gc_decode_range(C.byref(b), out.data_ptr(), ws.data_ptr(), ws.numel(), first,
+                                count, int(dgaps), _stream_ptr(stream))
+    if st:
+        raise GcError(st, "gc_decode_range")
 
 
 def decode_stage(batch: DeviceBatch, out, ws, dgaps: bool, stages: int, stream=None):

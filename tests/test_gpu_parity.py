@@ -259,3 +259,29 @@ def test_posting_store(codec, variant):
     for i in range(len(w.list_n)):
         o, n = int(st.list_out_off[i]), int(w.list_n[i])
         assert np.array_equal(got[o:o + n], w.values[starts[i]:starts[i] + n]), i
+
+
+@pytest.mark.parametrize("codec,variant", [(O.GROUP_SCHEME, O.gsc_variant(1, "CU")), (O.GROUP_PFD, 0),
+                                           (O.GROUP_AFOR, 0), (O.GROUP_SIMPLE, 0)])
+def test_decode_range_random_access(codec, variant):
+    """gc_decode_range (§8(f) rank 4): after one complete decode, random ranges decoded from
+    the workspace's per-tile skip table and carries equal the full decode on the covering
+    tiles and leave every other output position untouched (both paths)."""
+    w = gen.config(2, scale=1 / 32)
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, codec, variant))
+    db = gc.to_device(hb)
+    rng = np.random.default_rng(5)
+    T = 8192
+    for dgaps in (True, False):
+        full, ws = (gc.decode_dgaps if dgaps else gc.decode)(db)
+        full = full.clone()
+        for _ in range(6):
+            first = int(rng.integers(0, hb.total_out))
+            count = int(rng.integers(1, min(5 * T, hb.total_out - first) + 1))
+            out = torch.full((hb.total_out,), -7, dtype=torch.int32, device="cuda")
+            gc.decode_range(db, out, ws, first, count, dgaps)
+            torch.cuda.synchronize()
+            a, b = (first // T) * T, min(hb.total_out, -(-(first + count) // T) * T)
+            assert torch.equal(out[a:b], full[a:b]), (dgaps, first, count)
+            assert bool((out[:a] == -7).all()) and bool((out[b:] == -7).all())
+        assert gc.read_device_status(ws) == 0
