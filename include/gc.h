@@ -225,9 +225,9 @@ void gc_encode_abort(void* handle);
  * Group-PFD (variant 0) and SIMD-BP128 (PFD variant 1); bytes
  * identical to the host encoder's and the oracle's (every Group codec and variant;
  * GC_VARBYTE: GC_ERR_UNKNOWN_CODEC, use the host encoder; an invalid variant:
- * GC_ERR_BAD_VARIANT).  sizes[3] is an internal
- * count (frames, quads or blocks): pass sizes back to gc_encode_device_write unchanged.  All arrays are DEVICE memory except sizes[] and the
- * params struct.
+ * GC_ERR_BAD_VARIANT).  sizes[3] is an internal count (frames, quads or blocks): pass
+ * sizes back to gc_encode_device_write unchanged.  All arrays are DEVICE memory except
+ * sizes[] and the params struct.
  *   values[total_ints], list_n[n_lists]  as for gc_encode_begin (docIDs if delta)
  *   ws, ws_bytes         workspace of at least gc_encode_device_ws_size bytes,
  *                        256-B aligned, owned by the caller; shared by the two calls
