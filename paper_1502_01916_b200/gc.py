@@ -274,10 +274,15 @@ class PostingStore:
     list_out_off: np.ndarray   # uint64 [L]
     short_base: int
     total: int                 # ints of the decoded output (incl. the alignment gap)
+    tf_long: "HostBatch | None" = None    # term frequencies (raw, no d-gap), same split
+    tf_short: "HostBatch | None" = None
 
 
 def encode_posting_store(values: np.ndarray, list_n: np.ndarray, codec: int, variant: int = 0,
-                         delta: bool = False, threshold: int = 64, **kw) -> PostingStore:
+                         delta: bool = False, threshold: int = 64, tfs: "np.ndarray | None" = None,
+                         **kw) -> PostingStore:
+    """`tfs` (optional, one per posting): the lists' term frequencies, stored beside the
+    docIDs with the same split and codecs but no d-gap (TFs are not sorted)."""
     v = np.ascontiguousarray(values, np.uint32)
     ln = np.ascontiguousarray(list_n, np.uint32)
     starts = np.concatenate([[0], np.cumsum(ln.astype(np.int64))[:-1]]) if len(ln) else np.zeros(0, np.int64)
@@ -294,23 +299,52 @@ def encode_posting_store(values: np.ndarray, list_n: np.ndarray, codec: int, var
     off = np.zeros(len(ln), np.uint64)
     off[idx[False]] = longb.out_off[:-1]
     off[idx[True]] = short_base + shortb.out_off[:-1]
-    return PostingStore(longb, shortb, off, short_base, short_base + shortb.total_out)
+    st = PostingStore(longb, shortb, off, short_base, short_base + shortb.total_out)
+    if tfs is not None:
+        t = np.ascontiguousarray(tfs, np.uint32)
+        assert t.size == v.size, "one TF per posting"
+
+        def gather_t(ids):
+            if len(ids) == 0:
+                return np.zeros(0, np.uint32)
+            return np.concatenate([t[starts[i]:starts[i] + ln[i]] for i in ids])
+        st.tf_long = encode_batch(gather_t(idx[False]), ln[idx[False]], codec, variant, **kw)
+        st.tf_short = encode_batch(gather_t(idx[True]), ln[idx[True]], VARBYTE, 0)
+    return st
 
 
-def decode_posting_store(store: PostingStore, dgaps: bool = True, device="cuda", stream=None):
-    """Both groups decoded into one output (int32 view of uint32): the long group with its
-    codec, the short group with Variable Byte.  Returns (out, (ws_long, ws_short))."""
+def _decode_groups(batches, total, short_base, dgaps, device, stream):
     import torch
-    out = torch.empty(max(store.total, 4), dtype=torch.int32, device=device)
+    out = torch.empty(max(total, 4), dtype=torch.int32, device=device)
     fn = decode_dgaps if dgaps else decode
     wss = []
-    for hb, base in ((store.long, 0), (store.short, store.short_base)):
+    for hb, base in zip(batches, (0, short_base)):
         db = to_device(hb, device)
         ws = alloc_workspace(db, device)
         fn(db, out=out[base:base + max(hb.total_out, 4)] if hb.total_out else out, ws=ws,
            stream=stream)
         wss.append(ws)
-    return out[:store.total], tuple(wss)
+    return out[:total], tuple(wss)
+
+
+def decode_posting_store(store: PostingStore, dgaps: bool = True, device="cuda", stream=None):
+    """Both groups decoded into one output (int32 view of uint32): the long group with its
+    codec, the short group with Variable Byte.  Returns (out, (ws_long, ws_short)); with
+    TFs in the store, returns (docs, tfs, workspaces): the TFs (no d-gap) are decoded on a
+    second stream, concurrently with the docIDs (two decodes, not one fused kernel)."""
+    import torch
+    if store.tf_long is None:
+        return _decode_groups((store.long, store.short), store.total, store.short_base, dgaps,
+                              device, stream)
+    main = torch.cuda.current_stream(device) if stream is None else stream
+    tfs_stream = torch.cuda.Stream(device)
+    tfs_stream.wait_stream(main)
+    docs, w1 = _decode_groups((store.long, store.short), store.total, store.short_base, dgaps,
+                              device, main)
+    tfs, w2 = _decode_groups((store.tf_long, store.tf_short), store.total, store.short_base,
+                             False, device, tfs_stream)
+    main.wait_stream(tfs_stream)
+    return docs, tfs, w1 + w2
 
 
 def to_device(hb: HostBatch, device="cuda", pin: bool = False) -> DeviceBatch:

@@ -285,3 +285,23 @@ def test_decode_range_random_access(codec, variant):
             assert torch.equal(out[a:b], full[a:b]), (dgaps, first, count)
             assert bool((out[:a] == -7).all()) and bool((out[b:] == -7).all())
         assert gc.read_device_status(ws) == 0
+
+
+def test_posting_store_with_term_frequencies():
+    """The posting store with TF streams beside the docIDs (§8(f) rank 3): TFs (small, not
+    sorted: Geometric(0.5)) decoded raw, concurrently with the d-gap docIDs."""
+    w = gen.config(5, scale=2 ** -14)
+    rng = np.random.default_rng(9)
+    tfs = rng.geometric(0.5, w.n_ints).astype(np.uint32)
+    st = gc.encode_posting_store(w.values, w.list_n, O.GROUP_SCHEME, O.gsc_variant(8, "IU"),
+                                 delta=True, tfs=tfs)
+    docs, tf, wss = gc.decode_posting_store(st, dgaps=True)
+    torch.cuda.synchronize()
+    assert all(gc.read_device_status(ws) == 0 for ws in wss)
+    d = docs.cpu().numpy().view(np.uint32)
+    t = tf.cpu().numpy().view(np.uint32)
+    starts = np.concatenate([[0], np.cumsum(w.list_n.astype(np.int64))[:-1]])
+    for i in range(len(w.list_n)):
+        o, n = int(st.list_out_off[i]), int(w.list_n[i])
+        assert np.array_equal(d[o:o + n], w.values[starts[i]:starts[i] + n]), i
+        assert np.array_equal(t[o:o + n], tfs[starts[i]:starts[i] + n]), i
