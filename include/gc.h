@@ -60,7 +60,7 @@ typedef enum {
 /* GC_VARBYTE (P §2.3): the short-list fallback of P:L640 §7.5; its byte
  * stream (7-bit groups, least significant first, MSB = 1 on an int's last byte) is the
  * control area (ctrl / ctrl_off, byte offsets), there is no data area (data_off all 0);
- * decode and encode as the other codecs (no GPU encoder). */
+ * decoded and encoded (host and GPU) as the other codecs. */
 typedef enum { GC_VARBYTE = 1, GC_GROUP_SIMPLE = 2, GC_GROUP_SCHEME = 3, GC_GROUP_AFOR = 4,
                GC_GROUP_PFD = 5 } gc_codec;
 
@@ -220,12 +220,11 @@ gc_status gc_encode_finish(void* handle, uint8_t* ctrl, void* data, uint8_t* exc
 void gc_encode_abort(void* handle);
 
 /* ---------------------------------------------------------------------------
- * GPU encoders: Group-Simple (Algorithm 1),
- * Group-Scheme, all 10 variants, Group-AFOR,
+ * GPU encoders: Variable Byte (P §2.3), Group-Simple (Algorithm
+ * 1), Group-Scheme, all 10 variants, Group-AFOR,
  * Group-PFD (variant 0) and SIMD-BP128 (PFD variant 1); bytes
- * identical to the host encoder's and the oracle's (every Group codec and variant;
- * GC_VARBYTE: GC_ERR_UNKNOWN_CODEC, use the host encoder; an invalid variant:
- * GC_ERR_BAD_VARIANT).  sizes[3] is an internal count (frames, quads or blocks): pass
+ * identical to the host encoder's and the oracle's (every codec and variant the decoder
+ * takes; an invalid variant: GC_ERR_BAD_VARIANT).  sizes[3] is an internal count (frames, quads or blocks): pass
  * sizes back to gc_encode_device_write unchanged.  All arrays are DEVICE memory except
  * sizes[] and the params struct.
  *   values[total_ints], list_n[n_lists]  as for gc_encode_begin (docIDs if delta)

@@ -907,6 +907,74 @@ __global__ void k_gs_write(GsEnc E, const uint8_t* sel, const uint8_t* cov, cons
            (SEL << (4 * (s & 1))) << (8 * (uint32_t)(byte & 3)));
 }
 
+// ------------------------------------------------------------------ Variable Byte
+// P §2.3: an int takes ceil(width/7) bytes (width(0) = 1), 7-bit groups
+// least significant first, MSB = 1 on the last.  One thread per int: a global exclusive
+// scan of the byte lengths gives every int's position; per-list byte counts (differences of
+// the scan) padded to 4 and scanned over the lists give the directory.
+struct Vb {
+  const uint32_t* values;
+  const uint32_t* list_n;
+  uint64_t n_lists, n;
+  int delta;
+  uint64_t* out_off;   // [L+1]
+  uint8_t* len;        // [n] bytes per int
+  uint64_t* pos;       // [n+1] exclusive scan of len
+  uint64_t* cb;        // [L+1] control bytes per list (4-padded), then their scan
+};
+struct GetLen {
+  const uint8_t* p;
+  __device__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+__device__ __forceinline__ uint64_t vb_list_of(const Vb& V, uint64_t i) {
+  uint64_t a = 0, b = V.n_lists;  // the last list whose first int is <= i
+  while (b - a > 1) {
+    const uint64_t m = (a + b) >> 1;
+    if (V.out_off[m] <= i) a = m;
+    else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ uint32_t vb_value(const Vb& V, uint64_t i, uint64_t l) {
+  uint32_t x = V.values[i];
+  if (V.delta && i > V.out_off[l]) x -= V.values[i - 1];  // d-gaps
+  return x;
+}
+__global__ void k_vb_len(Vb V) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V.n) return;
+  const uint32_t x = vb_value(V, i, vb_list_of(V, i));
+  V.len[i] = (uint8_t)((width_of(x) + 6) / 7);
+}
+__global__ void k_vb_sizes(Vb V) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= V.n_lists) return;
+  const uint64_t bytes = V.pos[V.out_off[l + 1]] - V.pos[V.out_off[l]];
+  V.cb[l] = 4 * ((bytes + 3) / 4);
+}
+__global__ void k_vb_write(Vb V, const uint64_t* ctrl_off, uint8_t* ctrl) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V.n) return;
+  const uint64_t l = vb_list_of(V, i);
+  uint32_t x = vb_value(V, i, l);
+  uint64_t p = ctrl_off[l] + (V.pos[i] - V.pos[V.out_off[l]]);
+  const uint32_t k = V.len[i];
+  for (uint32_t j = 0; j < k; j++, x >>= 7) ctrl[p + j] = (uint8_t)((x & 127u) | (j + 1 == k ? 128u : 0u));
+}
+struct VbWs {
+  uint64_t len, pos, cb, sums, bytes;
+};
+inline VbWs vb_ws_layout(uint64_t n_lists, uint64_t total) {
+  auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
+  VbWs L;
+  L.len = 0;
+  L.pos = al(total + 1);
+  L.cb = L.pos + al(8 * (total + 1));
+  L.sums = L.cb + al(8 * (n_lists + 1));
+  L.bytes = L.sums + al(8 * ((std::max(total, n_lists) + 1) / kScanB + 3));
+  return L;
+}
+
 struct GscWs {
   uint64_t quad_off, u, bw_off, cu_off, c_off, d_off, ch_off, adv, start, lstart, lid, sums, bytes;
 };
@@ -955,6 +1023,23 @@ bool is_gsc(const gc_encode_params* p) {  // binary, complete unary, incomplete 
 }
 bool is_afor(const gc_encode_params* p) { return p->codec == GC_GROUP_AFOR; }
 bool is_gs(const gc_encode_params* p) { return p->codec == GC_GROUP_SIMPLE; }
+bool is_vb(const gc_encode_params* p) { return p->codec == GC_VARBYTE; }
+Vb make_vb(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists, uint64_t total,
+           int delta, uint64_t* out_off, void* ws) {
+  const VbWs L = vb_ws_layout(n_lists, total);
+  uint8_t* w = (uint8_t*)ws;
+  Vb V;
+  V.values = values;
+  V.list_n = list_n;
+  V.n_lists = n_lists;
+  V.n = total;
+  V.delta = delta;
+  V.out_off = out_off;
+  V.len = w + L.len;
+  V.pos = (uint64_t*)(w + L.pos);
+  V.cb = (uint64_t*)(w + L.cb);
+  return V;
+}
 gc_status refuse(const gc_encode_params* p) {
   if (!p) return GC_ERR_INVALID_ARGUMENT;
   if (p->codec != GC_GROUP_PFD && p->codec != GC_GROUP_SCHEME) return GC_ERR_UNKNOWN_CODEC;
@@ -1069,6 +1154,7 @@ gc_status gc_encode_device_ws_size(const gc_encode_params* p, uint64_t n_lists, 
   else if (is_gsc(p)) *bytes = gsc_ws_layout(n_lists, total_ints).bytes;
   else if (is_afor(p)) *bytes = afor_ws_layout(n_lists, total_ints).bytes;
   else if (is_gs(p)) *bytes = gs_ws_layout(n_lists, total_ints).bytes;
+  else if (is_vb(p)) *bytes = vb_ws_layout(n_lists, total_ints).bytes;
   else return refuse(p);
   return GC_OK;
 }
@@ -1135,6 +1221,39 @@ static gc_status gsc_plan(const gc_encode_params* p, const uint32_t* values, con
   sizes[1] = vt;
   sizes[2] = 0;
   sizes[3] = nq;
+  return GC_OK;
+}
+
+static gc_status vb_plan(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists,
+                         uint64_t total_ints, int delta, uint64_t* ctrl_off, uint64_t* data_off,
+                         uint64_t* exc_off, uint64_t* out_off, void* ws, uint64_t* sizes,
+                         cudaStream_t st) {
+  const VbWs L = vb_ws_layout(n_lists, total_ints);
+  Vb V = make_vb(values, list_n, n_lists, total_ints, delta, out_off, ws);
+  uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
+  if (scan_u64(GetListN{list_n}, n_lists, out_off, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  uint64_t tot = 0;
+  if (cudaMemcpyAsync(&tot, out_off + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  if (tot != total_ints) return GC_ERR_INVALID_ARGUMENT;
+  if (total_ints) k_vb_len<<<(unsigned)((total_ints + 255) / 256), 256, 0, st>>>(V);
+  if (scan_u64(GetLen{V.len}, total_ints, V.pos, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  if (n_lists) k_vb_sizes<<<(unsigned)((n_lists + 255) / 256), 256, 0, st>>>(V);
+  if (scan_u64(GetArr{V.cb}, n_lists, V.cb, sums, st) != cudaSuccess) return GC_ERR_CUDA;
+  const unsigned nbl = (unsigned)((n_lists + 1 + 255) / 256);
+  k_copy_u64<<<nbl, 256, 0, st>>>(V.cb, ctrl_off, n_lists + 1);
+  if (cudaMemsetAsync(data_off, 0, 8 * (n_lists + 1), st) != cudaSuccess ||
+      cudaMemsetAsync(exc_off, 0, 8 * (n_lists + 1), st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  uint64_t ct = 0;
+  if (cudaMemcpyAsync(&ct, V.cb + n_lists, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return GC_ERR_CUDA;
+  sizes[0] = 16 * ((ct + 15) / 16);
+  sizes[1] = 0;
+  sizes[2] = 0;
+  sizes[3] = total_ints;
   return GC_OK;
 }
 
@@ -1243,6 +1362,9 @@ gc_status gc_encode_device_plan(const gc_encode_params* p, const uint32_t* value
   if (is_gs(p))
     return gs_plan(values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
                    out_off, ws, sizes, st);
+  if (is_vb(p))
+    return vb_plan(values, list_n, n_lists, total_ints, delta, ctrl_off, data_off, exc_off,
+                   out_off, ws, sizes, st);
   const WsLayout L = ws_layout(n_lists, total_ints, p->pfd_frame_quads);
   Dir D = make_dir(p, values, list_n, n_lists, delta, out_off, ws, total_ints);
   uint64_t* sums = (uint64_t*)((uint8_t*)ws + L.sums);
@@ -1303,6 +1425,14 @@ gc_status gc_encode_device_write(const gc_encode_params* p, const uint32_t* valu
       k_gsc_write<<<(unsigned)((G.n_quads + 255) / 256), 256, 0, st>>>(
           G, (const uint64_t*)((uint8_t*)ws + L.c_off), (const uint64_t*)((uint8_t*)ws + L.d_off),
           ctrl, (uint32_t*)data);
+    return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  }
+  if (is_vb(p)) {
+    const VbWs L = vb_ws_layout(n_lists, total_ints);
+    Vb V = make_vb(values, list_n, n_lists, total_ints, delta, const_cast<uint64_t*>(out_off), ws);
+    if (total_ints)
+      k_vb_write<<<(unsigned)((total_ints + 255) / 256), 256, 0, st>>>(
+          V, (const uint64_t*)((uint8_t*)ws + L.cb), ctrl);
     return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
   }
   if (is_gs(p)) {

@@ -173,6 +173,17 @@ def test_group_simple():
     check_stream_codec(w.values, w.list_n, O.GROUP_SIMPLE, delta=True)
 
 
+def test_varbyte():
+    """Variable Byte (P §2.3) encoded on the device: random lists, docIDs in (config 5's
+    shape: most lists short), byte-identical to the oracle."""
+    rng = np.random.default_rng(95)
+    for n_lists, max_len, bits in ((1, 3, 1), (300, 80, 14), (40, 3000, 32)):
+        w = gen.random_lists(rng, n_lists, max_len, bits)
+        check_stream_codec(w.values, w.list_n, O.VARBYTE)
+    w = gen.config(5, scale=2 ** -15)
+    check_stream_codec(w.values, w.list_n, O.VARBYTE, delta=True)
+
+
 def test_other_codecs_refused():
     v = torch.zeros(16, dtype=torch.int32, device="cuda")
     ln = torch.tensor([16], dtype=torch.int32, device="cuda")
@@ -181,7 +192,8 @@ def test_other_codecs_refused():
             gc.encode_device(v, ln, codec, variant)
 
 
-ALL_CODECS = ([(O.GROUP_SIMPLE, 0), (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0), (O.GROUP_PFD, 1)]
+ALL_CODECS = ([(O.VARBYTE, 0), (O.GROUP_SIMPLE, 0), (O.GROUP_AFOR, 0), (O.GROUP_PFD, 0),
+               (O.GROUP_PFD, 1)]
               + [(O.GROUP_SCHEME, O.gsc_variant(cg, k)) for cg, k in GSC_BCU])
 
 
