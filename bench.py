@@ -78,6 +78,20 @@ def config_codecs(k: int, zeta):
             (gc.GROUP_PFD, 0, 32, zeta), (gc.VARBYTE, 0, 32, zeta)]
 
 
+def codec_subset(w, codec: int):
+    """The lists a codec decodes in a step: all of them, except Variable Byte, which is the
+    short-list fallback (§7.5): the lists shorter than 64."""
+    from paper_1502_01916_b200 import gc
+    if codec != gc.VARBYTE:
+        return w.values, w.list_n
+    ln = w.list_n.astype(np.int64)
+    st = np.concatenate([[0], np.cumsum(ln)[:-1]]) if len(ln) else np.zeros(0, np.int64)
+    ids = np.nonzero(w.list_n < 64)[0]
+    vals = (np.concatenate([w.values[st[i]:st[i] + ln[i]] for i in ids]) if len(ids)
+            else np.zeros(0, np.uint32))
+    return vals, w.list_n[ids]
+
+
 def make_workload(args, rank, world):
     """(workload, global id of its first list, scaling) of this rank (dist.shard_for_rank)."""
     from paper_1502_01916_b200 import dist
@@ -187,7 +201,7 @@ def run_reference(args, rank, world):
     O.build()
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
     w, _, scaling = make_workload(args, 0, 1)
-    hbs = [gc.encode_batch(w.values, w.list_n, c, v, delta=w.delta, frame_quads=f, zeta=z)
+    hbs = [gc.encode_batch(*codec_subset(w, c), c, v, delta=w.delta, frame_quads=f, zeta=z)
            for c, v, f, z in config_codecs(args.config, zeta)]
     threads = len(os.sched_getaffinity(0))
     frac = min(1.0, 2.0e6 / max(1, w.n_ints))     # ~2M ints per variant per step
@@ -328,16 +342,7 @@ def main():
     t_setup = time.perf_counter()
     w, list_base, scaling = make_workload(args, rank, world)
 
-    def subset(c):  # Variable Byte is the short-list fallback (§7.5): lists < 64
-        if c != gc.VARBYTE:
-            return w.values, w.list_n
-        ln = w.list_n.astype(np.int64)
-        st = np.concatenate([[0], np.cumsum(ln)[:-1]])
-        ids = np.nonzero(w.list_n < 64)[0]
-        vals = (np.concatenate([w.values[st[i]:st[i] + ln[i]] for i in ids]) if len(ids)
-                else np.zeros(0, np.uint32))
-        return vals, w.list_n[ids]
-    subs = [subset(c) for c, _, _, _ in codecs]
+    subs = [codec_subset(w, c) for c, _, _, _ in codecs]
     hbs = [gc.encode_batch(sv, sl, c, v, delta=w.delta, frame_quads=f, zeta=z)
            for (sv, sl), (c, v, f, z) in zip(subs, codecs)]
     dbs = [gc.to_device(hb, dev) for hb in hbs]
