@@ -370,19 +370,9 @@ struct GetU {
   const uint8_t* u;
   __device__ uint64_t operator()(uint64_t i) const { return u[i]; }
 };
-__device__ __forceinline__ uint64_t list_of_quad(const Gsc& G, uint64_t g) {
-  uint64_t a = 0, b = G.n_lists;  // the last list whose first quad is <= g
-  while (b - a > 1) {
-    const uint64_t m = (a + b) >> 1;
-    if (G.quad_off[m] <= g) a = m;
-    else b = m;
-  }
-  return a;
-}
-// the list of quad g for a full warp of consecutive quads: one binary search (lane 0, the
-// warp's first quad), then every lane steps forward over the few list starts in between
-__device__ __forceinline__ uint64_t warp_list_of_quad(const Gsc& G, uint64_t g) {
-  return g < G.n_quads ? G.lid[g + 1] : 0;  // (precomputed, no search)
+// the list of quad g (lid: the scan of the list-start counts, k_gsc_lstart)
+__device__ __forceinline__ uint64_t quad_list(const Gsc& G, uint64_t g) {
+  return g < G.n_quads ? G.lid[g + 1] : 0;
 }
 __device__ __forceinline__ void gsc_quad(const Gsc& G, uint64_t l, uint64_t j, uint32_t* v) {
   const uint32_t n = G.list_n[l];
@@ -400,7 +390,7 @@ __device__ __forceinline__ void gsc_quad(const Gsc& G, uint64_t l, uint64_t j, u
 }
 __global__ void k_gsc_units(Gsc G) {
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t l = warp_list_of_quad(G, g);
+  const uint64_t l = quad_list(G, g);
   if (g >= G.n_quads) return;
   uint32_t v[4];
   gsc_quad(G, l, g - G.quad_off[l], v);
@@ -418,7 +408,7 @@ __global__ void k_gsc_sizes(Gsc G, uint64_t* cb, uint64_t* vecs) {
   } else {  // A18: CG 1 three 5-bit fields per 16-bit unit, CG 2/4 two per byte, CG 8 four
     bytes = G.cg == 1 ? 2 * ((Q + 2) / 3) : (G.cg == 8 ? (Q + 3) / 4 : (Q + 1) / 2);
   }
-  if (G.kind != 2) cb[l] = 4 * ((bytes + 3) / 4);  // (IU: k_gsc_iu_pos)
+  if (G.kind != 2) cb[l] = 4 * ((bytes + 3) / 4);  // (IU: k_iu_chain)
   vecs[l] = (G.bw_off[qe] - G.bw_off[qs] + 31) / 32;
 }
 // incomplete unary (A17): a code never crosses a byte -- if it does not fit in the rest of
@@ -540,7 +530,7 @@ __global__ void __launch_bounds__(256) k_gsc_write(Gsc G, const uint64_t* ctrl_o
   const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool act = g < G.n_quads;
-  const uint64_t lw = warp_list_of_quad(G, g);
+  const uint64_t lw = quad_list(G, g);
   uint64_t pos = 0;
   uint32_t bw = 0, v[4] = {0, 0, 0, 0};
   if (act) {
