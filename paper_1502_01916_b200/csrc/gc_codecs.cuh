@@ -19,6 +19,9 @@
 
 #include "gc_device.cuh"
 
+#ifndef GC_FRAME_UPT
+#define GC_FRAME_UPT 2  // parse units per thread per chunk for the frame codecs (AFOR, PFD)
+#endif
 #ifndef GC_CU8_PARTS
 #define GC_CU8_PARTS 2
 #endif
@@ -383,6 +386,7 @@ struct CodecAFOR {
   static constexpr bool kExc = false;
   static constexpr uint64_t kBackBits = 0;
   static constexpr int kParts = 4;           // a parse unit = one frame header byte
+  static constexpr uint32_t kUnitsPerThread = GC_FRAME_UPT;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
@@ -420,6 +424,7 @@ template <int F, bool kE = true>
 struct CodecPFD {
   static constexpr bool kExc = kE;
   static constexpr uint32_t kFrameQuads = F;
+  static constexpr uint32_t kUnitsPerThread = GC_FRAME_UPT;
   static constexpr uint64_t kBackBits = 0;
   static constexpr int kParts = F / 8;        // a parse unit = 8 quads of one frame
   static constexpr bool kNeedsPrev = false;

@@ -88,6 +88,17 @@ struct Geo {
   Seg4 seed;  // (list start flag, raw quads, data lane-bits, exception bytes) at word wa
 };
 
+// Parse units per thread per parse chunk: kUPT, or a codec's own kUnitsPerThread (the
+// frame codecs, whose units are whole 8..32-quad frame parts, balance better with 2).
+template <class C, class = void>
+struct UnitsPerThread {
+  static constexpr uint32_t v = kUPT;
+};
+template <class C>
+struct UnitsPerThread<C, std::void_t<decltype(C::kUnitsPerThread)>> {
+  static constexpr uint32_t v = C::kUnitsPerThread;
+};
+
 #ifndef GC_DECODE_MINB
 #define GC_DECODE_MINB 3
 #endif
@@ -117,6 +128,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
   __shared__ uint32_t s_reset0[2], s_cin;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t kU = UnitsPerThread<C>::v;  // parse units per thread per parse chunk
   const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
   const uint64_t dend = D.data_off[D.n_lists];
   const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
@@ -377,7 +389,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       constexpr uint32_t P = C::kParts;
       const uint32_t ru0 = rw0 * P, ru1 = rw1 * P;
       const uint32_t nu = ru1 > ru0 ? ru1 - ru0 : 0u;
-      const uint32_t ku = max(1u, min(kUPT, (nu + kDT - 1) / kDT));
+      const uint32_t ku = max(1u, min(kU, (nu + kDT - 1) / kDT));
       Seg4 carry = lr == 0 ? seed : Seg4{0u, 0u, 0u, 0u};
       for (uint32_t cb0 = ru0; cb0 < ru1; cb0 += kDT * ku) {
         const uint32_t my0 = cb0 + tid * ku;
@@ -393,11 +405,11 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
           }
           li = a;
         }
-        uint32_t wv[kUPT], pv[kUPT], wl[kUPT];
-        WAgg wg[kUPT];
+        uint32_t wv[kU], pv[kU], wl[kU];
+        WAgg wg[kU];
         Seg4 agg{0u, 0u, 0u, 0u};
 #pragma unroll
-        for (uint32_t k = 0; k < kUPT; k++) {
+        for (uint32_t k = 0; k < kU; k++) {
           wv[k] = pv[k] = 0u;
           wl[k] = li;
           wg[k] = WAgg{0u, 0u, 0u};
@@ -424,7 +436,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
         }
         auto units = [&](auto staged) {
 #pragma unroll
-          for (uint32_t k = 0; k < kUPT; k++) {
+          for (uint32_t k = 0; k < kU; k++) {
             if (k >= myn) break;
             const uint32_t un = my0 + k, w = un / P, part = un % P;
             const uint32_t i = wl[k];
