@@ -166,7 +166,9 @@ gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t w
  * gc_decode (dgaps == 0) / gc_decode_dgaps (dgaps != 0) of the same batch: its per-tile
  * entries (control word, quad / data / exception prefixes) are the skip table and its
  * per-tile inclusive d-gap prefixes the carries, so neither the reset nor the index stage
- * runs.  Not for GC_VARBYTE (GC_ERR_UNKNOWN_CODEC).  Asynchronous on `stream`. */
+ * runs.  A d-gap range from a workspace without a complete gc_decode_dgaps sets
+ * GC_DEV_TRUNCATED and decodes nothing (it never waits).  Not for GC_VARBYTE
+ * (GC_ERR_UNKNOWN_CODEC).  Asynchronous on `stream`. */
 gc_status gc_decode_range(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           uint64_t first, uint64_t count, int dgaps, void* stream);
 

@@ -129,6 +129,12 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t kU = UnitsPerThread<C>::v;  // parse units per thread per parse chunk
+  // a range decode reads the carries a complete d-gap decode left: without one it would
+  // wait forever on unpublished tiles -- flag it instead (the flag cannot change meanwhile)
+  if (DGAPS && D.need_ready && ld_relaxed_u32(&D.hdr->dgaps_ready) == 0) {
+    if (tid == 0 && blockIdx.x == 0) atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
+    return;
+  }
   const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
   const uint64_t dend = D.data_off[D.n_lists];
   const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
@@ -621,6 +627,15 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     GC_T(7);
   }
   if (DGAPS && s_pend.on) flush_pending();
+  // the last CTA of a complete d-gap decode marks the workspace's carries usable for
+  // gc_decode_range (every CTA has published all its tiles before it counts itself)
+  if (DGAPS && !D.need_ready && D.tile_begin == 0 && D.tile_end == D.n_tiles_b) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(&D.hdr->counter_b, 1u) == gridDim.x - 1) st_relaxed_u32(&D.hdr->dgaps_ready, 1u);
+    }
+  }
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);
 }

@@ -49,7 +49,9 @@ struct Dev {
   Entry* entries;
   uint32_t* first_list;   // [n_tiles_a] 1 + owner list of the first word of control tile a
   uint32_t tile_begin, tile_end;  // k_decode: the output tiles to decode (gc_decode_range)
+  uint32_t need_ready;            // a range decode: the carries must come from a full decode
 };
+
 
 // Per-list view used by the group walks of the index kernel.
 struct ListCur {
@@ -776,6 +778,7 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
   D.entries = (Entry*)(w + L.off_entries);
   D.first_list = (uint32_t*)(w + L.off_first);
+  D.need_ready = range_count != ~0ull ? 1u : 0u;
   D.tile_begin = (uint32_t)mn64(range_first / kT, L.n_tiles_b);
   D.tile_end = (uint32_t)(range_count == ~0ull ? L.n_tiles_b
                                                : mn64((range_first + range_count + kT - 1) / kT, L.n_tiles_b));

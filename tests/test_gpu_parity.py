@@ -305,3 +305,16 @@ def test_posting_store_with_term_frequencies():
         o, n = int(st.list_out_off[i]), int(w.list_n[i])
         assert np.array_equal(d[o:o + n], w.values[starts[i]:starts[i] + n]), i
         assert np.array_equal(t[o:o + n], tfs[starts[i]:starts[i] + n]), i
+
+
+def test_decode_range_without_full_decode_is_flagged_not_hung():
+    """A d-gap range decode from a workspace that never held a complete d-gap decode has no
+    carries: it must flag the workspace (GC_DEV_TRUNCATED) and return, not wait."""
+    w = gen.config(2, scale=1 / 64)
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME, 0))
+    db = gc.to_device(hb)
+    _, ws = gc.decode(db)                    # gaps only: no carries published
+    out = torch.zeros(hb.total_out, dtype=torch.int32, device="cuda")
+    gc.decode_range(db, out, ws, 9000, 100, dgaps=True)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) & 16
