@@ -6,13 +6,18 @@ on B200 (BASELINE.json metric), one JSON line on rank 0.
 
 A step is one pass of the whole hot path (control scan, unpack, PFD patch, d-gap scan,
 store: gc_decode_dgaps) over one batch for every codec variant of the config.  The
-default workload is BASELINE.json configs[1]: Group-Scheme, all 10 granularity x
-length-descriptor variants, 2^26 ints in 10^5 lists.  Inputs are synthetic (gen/), encoded
-by the library's own host encoder, resident in HBM before timing; every working set
-(>= 380 MB per variant) is larger than the 126 MB L2.  Multi-GPU: one process per GPU
-(torchrun), lists sharded by rank (weak scaling: each rank decodes its own replica of the
-config), no collective on the data path; NCCL all-reduces counts and checksums after
-timing and the max time over ranks.
+headline workload (`value`) is BASELINE.json configs[1]: Group-Scheme, all 10 granularity x
+length-descriptor variants, 2^26 ints in 10^5 lists.  The same run times the other
+single-GPU configs at full size as well -- config 1 (Group-Simple, L2-flushed), config 3
+(Group-PFD, SIMD-BP128), config 4 (Group-AFOR) -- so `per_codec` holds all 13 variants
+("per codec", the metric's own words).  Inputs are synthetic (gen/), encoded by the
+library's own host encoder, resident in HBM before timing.
+
+Multi-GPU: `--gpus N` starts N ranks itself (torch.distributed.run) unless it already runs
+under one.  One process per GPU, lists sharded by rank with no collective on the data
+path; with N > 1 the workload is config 5 (rank r decodes shard r of its 8 list shards,
+weak scaling: N = 8 is exactly config 5).  NCCL all-reduces counts and checksums after
+timing and the max time over ranks; a barrier precedes every timed step.
 """
 from __future__ import annotations
 
@@ -38,7 +43,11 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
+                    help="headline workload (default: 2 on one GPU, 5 on several)")
+    ap.add_argument("--extra-configs", default="auto",
+                    help="configs timed beside the headline for per_codec ('auto': 1,3,4 "
+                         "when the headline is config 2 on one GPU; 'none')")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--codecs", default="", help="comma list of labels (default: config's)")
     ap.add_argument("--pfd-zeta", default="1/10")
@@ -61,12 +70,26 @@ def dist_info():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
 
 
+def label_of(codec: int, variant: int, frame_quads: int = 32) -> str:
+    """gc.codec_label without importing the product package (the reference arm)."""
+    import oracle as O
+    if codec == O.GROUP_SCHEME:
+        cg, kind = 1 << (variant & 3), ("B", "CU", "IU")[(variant >> 2) & 3]
+        return f"GSC-{cg}-{kind}"
+    name = {O.VARBYTE: "VByte", O.GROUP_SIMPLE: "G-SIM", O.GROUP_AFOR: "G-AFOR"}.get(codec)
+    if name:
+        return name
+    base = "BP128" if variant == 1 else "G-PFD"
+    return base if frame_quads == 32 else f"{base}-F{frame_quads}"
+
+
 def config_codecs(k: int, zeta):
-    from paper_1502_01916_b200 import gc
+    import oracle as gc  # (the codec ids; no product code on the reference arm)
     if k == 1:
         return [(gc.GROUP_SIMPLE, 0, 32, zeta)]
     if k == 2:
-        return [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd), 32, zeta) for cg, kd in gc.GSC_VARIANTS]
+        return [(gc.GROUP_SCHEME, gc.gsc_variant(cg, kd), 32, zeta)
+                for cg, kd in [(cg, k) for cg in (1, 2, 4, 8) for k in ("B", "CU")] + [(4, "IU"), (8, "IU")]]
     if k == 3:  # + SIMD-BP128 (P:L424) on the same gaps: the paper's speed leader as a control
         return [(gc.GROUP_PFD, 0, 32, zeta), (gc.GROUP_PFD, 1, 32, zeta)]
     if k == 4:
@@ -155,13 +178,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_decode launch from the committed
-    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+def ncu_traffic(workload: str, label: str):
+    """Measured DRAM + L2 traffic of one k_decode launch of this workload and variant, from
+    the committed ncu --set full capture (profiles/r2_traffic.json, written by
+    scripts/ncu_summary.py traffic): dram__bytes_read.sum + 32 x
+    lts__t_sectors_srcunit_tex_op_write.sum (the writes reach L2 in full even when the tail
+    is still in L2 at the kernel's end), or None when no capture exists."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             t = json.load(f)
-        return t.get(workload)
+        return t.get(workload, {}).get(label)
     except Exception:  # noqa: BLE001
         return None
 
@@ -193,36 +219,50 @@ def cpu_oracle_rate(hbs, frac_lists: float, budget_s: float, threads: int):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, on the
+    headline config: every step decodes, for each variant, the first lists of the batch
+    (about 2M ints) encoded by the oracle's own encoder -- no product code on this path."""
     if rank != 0:
         return
-    from paper_1502_01916_b200 import gc
     import oracle as O
     O.build()
+    if args.config == 0:
+        args.config = 5 if world > 1 else 2
     zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
     w, _, scaling = make_workload(args, 0, 1)
-    hbs = [gc.encode_batch(*codec_subset(w, c), c, v, delta=w.delta, frame_quads=f, zeta=z)
-           for c, v, f, z in config_codecs(args.config, zeta)]
     threads = len(os.sched_getaffinity(0))
-    frac = min(1.0, 2.0e6 / max(1, w.n_ints))     # ~2M ints per variant per step
+    labels, samples = [], []
+    for c, v, f, z in config_codecs(args.config, zeta):
+        sv, sl = codec_subset(w, c)
+        cs = np.cumsum(sl.astype(np.int64))
+        nl = max(1, int(np.searchsorted(cs, min(int(cs[-1]) if len(cs) else 0, 2_000_000)) + 1))
+        nl = min(nl, len(sl))
+        ns = int(cs[nl - 1]) if nl else 0
+        samples.append(O.encode_batch(sv[:ns], sl[:nl], c, v, delta=w.delta, frame_quads=f,
+                                      zeta=z, threads=threads))
+        labels.append(label_of(c, v, f))
+    outs = [np.empty(max(int(s["total_out"]), 1), np.uint32) for s in samples]
+    n_step = sum(int(s["total_out"]) for s in samples)
+
+    def one_step():
+        for smp, o in zip(samples, outs):
+            O.decode_batch(smp, dgaps=True, threads=threads, out=o)
     for _ in range(args.warmup):
-        cpu_oracle_rate(hbs, frac, 0.0, threads)
+        one_step()
     t0 = time.perf_counter()
-    n_step = 0
     for _ in range(args.steps):
-        _, n_step, _, _ = cpu_oracle_rate(hbs, frac, 0.0, threads)
+        one_step()
     dt = time.perf_counter() - t0
     value = n_step * args.steps / dt
-    sample = (f"first {frac:.4f} of the lists of each of {len(hbs)} batches "
-              f"({n_step} ints per step)")
+    sample = (f"the first lists (~2M ints) of each of the {len(samples)} variants' batches, "
+              f"{n_step} ints per step, encoded by the oracle (gco_encode_batch) and decoded "
+              "by gco_decode_batch with the d-gap prefix sum")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "config": {"workload": w.name, "n_ints": w.n_ints,
-                                        "n_lists": int(len(w.list_n)),
-                                        "codecs": [gc.codec_label(c, v, f) for c, v, f, _ in
-                                                   config_codecs(args.config, zeta)]},
+                                        "n_lists": int(len(w.list_n)), "codecs": labels},
         "cpu_baseline": {"kind": "oracle", "cores": threads, "sample": sample, "value": value,
                          "unit": "ints/s"},
         "e2e": {"value": value, "unit": "ints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -306,48 +346,39 @@ def run_encode(args, dev):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse_args()
-    rank, local_rank, world = dist_info()
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
-    if args.encode:
-        import torch
-        from paper_1502_01916_b200 import build
-        build.build()
-        torch.cuda.set_device(local_rank)
-        if rank == 0:
-            run_encode(args, torch.device("cuda", local_rank))
-        return
+def maybe_spawn(args):
+    """--gpus N outside torchrun: re-run this script as N ranks (torch.distributed.run,
+    127.0.0.1 rendezvous).  Returns True when the ranks ran here (the caller exits)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # the communicator's nranks in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd, env=env)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
+def time_variants(args, w, codecs, dev, pg, steps, warmup, headline):
+    """Encode (host encoder), upload, verify and time every variant of one workload.
+    Returns a dict with the per-variant timings and, for the headline, the step timing."""
     import torch
-    from paper_1502_01916_b200 import build
-    build.build()
     from paper_1502_01916_b200 import gc
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
-    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
-    codecs = config_codecs(args.config, zeta)
-    if args.codecs:
-        keep = set(args.codecs.split(","))
-        codecs = [c for c in codecs if gc.codec_label(c[0], c[1], c[2]) in keep]
-
-    # ---- inputs (untimed): generate, encode with the library's host encoder, copy to HBM
     t_setup = time.perf_counter()
-    w, list_base, scaling = make_workload(args, rank, world)
-
     subs = [codec_subset(w, c) for c, _, _, _ in codecs]
     hbs = [gc.encode_batch(sv, sl, c, v, delta=w.delta, frame_quads=f, zeta=z)
            for (sv, sl), (c, v, f, z) in zip(subs, codecs)]
     dbs = [gc.to_device(hb, dev) for hb in hbs]
-    n_ints = max(hb.total_out for hb in hbs)          # (the largest batch)
-    n_ints_all = sum(hb.total_out for hb in hbs)      # ints decoded per step
+    n_ints = max(hb.total_out for hb in hbs)
     out = torch.empty(max(n_ints, 4), dtype=torch.int32, device=dev)
     wss = [gc.alloc_workspace(db, dev) for db in dbs]
     stream = torch.cuda.current_stream(dev)
@@ -372,15 +403,14 @@ def main():
             ok = bool(torch.equal(docs, vals)) if w.delta else bool(torch.equal(g, vals))
             if ok_g is False or not ok or st:
                 verified = False
-                print(f"[rank {rank}] PARITY FAILURE {lab}: gaps={ok_g} docs={ok} status="
+                print(f"PARITY FAILURE {w.name} {lab}: gaps={ok_g} docs={ok} status="
                       f"{gc.status_names(st)}", file=sys.stderr)
-        del vals
+            del vals, g
     t_setup = time.perf_counter() - t_setup
 
     # ---- timed region: K steps x all variants of gc_decode_dgaps (stage events per launch)
-    # per variant: index start / end, decode start / end
     ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in dbs]
-          for _ in range(args.steps)]
+          for _ in range(steps)]
     sides = [torch.cuda.Stream(dev) for _ in range(max(1, args.side_streams))]
 
     def step(evs=None):
@@ -420,43 +450,47 @@ def main():
         for side in sides:
             stream.wait_stream(side)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
-    torch.cuda.synchronize(dev)
-    if pg:
-        pg.barrier()
     torch.cuda.synchronize(dev)
     # a working set that fits in L2 is flushed before every timed step (a scratch write of
     # 4x the L2), and only the steps are timed; larger ones need no flush
     l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20))
     algo_ws = [hb.compressed_bytes + 4 * hb.total_out + hb.directory_bytes for hb in hbs]
     flush = torch.empty(4 * l2_bytes, dtype=torch.uint8, device=dev) if max(algo_ws) < l2_bytes else None
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clk:
-        t0.record(stream)
-        for k in range(args.steps):
-            if flush is not None:
-                flush.fill_(k & 0xFF)
-            step_ev[k][0].record(stream)
-            step(ev[k])
-            step_ev[k][1].record(stream)
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
+               for _ in range(steps)]
+    clk = ClockSampler(torch.cuda.current_device()) if headline else None
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
-    ms = sum(a.elapsed_time(b) for a, b in step_ev)  # (the steps only; equals t1 - t0 unflushed)
+    if clk:
+        clk.__enter__()
+    for k in range(steps):
+        if flush is not None:
+            flush.fill_(k & 0xFF)
+        if pg:  # every rank starts the step together (the per-step barrier)
+            torch.cuda.synchronize(dev)
+            pg.barrier()
+        step_ev[k][0].record(stream)
+        step(ev[k])
+        step_ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if clk:
+        clk.__exit__()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    ms = sum(a.elapsed_time(b) for a, b in step_ev)  # (the steps only)
     small_extra = None
     if flush is not None:  # L2-warm and CUDA-graph numbers, labelled
         w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         w1.record(stream)
         torch.cuda.synchronize(dev)
-        small_extra = {"l2_warm_ms_per_step": w0.elapsed_time(w1) / args.steps}
+        small_extra = {"l2_warm_ms_per_step": w0.elapsed_time(w1) / steps}
         try:
             def serial_step():  # the same stages on the capturing stream
                 for db, ws in zip(dbs, wss):
@@ -474,43 +508,136 @@ def main():
             graph.replay()
             torch.cuda.synchronize(dev)
             w0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 graph.replay()
             w1.record(stream)
             torch.cuda.synchronize(dev)
-            small_extra["cuda_graph_l2_warm_ms_per_step"] = w0.elapsed_time(w1) / args.steps
+            small_extra["cuda_graph_l2_warm_ms_per_step"] = w0.elapsed_time(w1) / steps
         except Exception as e:  # noqa: BLE001
             small_extra["cuda_graph"] = f"capture failed: {e}"[:200]
-    dec_ms = [sum(ev[k][i][2].elapsed_time(ev[k][i][3]) for k in range(args.steps)) / args.steps
+    dec_ms = [sum(ev[k][i][2].elapsed_time(ev[k][i][3]) for k in range(steps)) / steps
               for i in range(len(dbs))]
-    idx_ms = [sum(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)) / args.steps
+    idx_ms = [sum(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(steps)) / steps
               for i in range(len(dbs))]
     step_ms = sorted(a.elapsed_time(b) for a, b in step_ev)
 
-    # ---- gc_decode (gaps only, the paper's measured path, A38) beside it: k_decode without
-    # the d-gap scan, same variants, same repetitions (untimed for the headline)
+    # ---- gc_decode (gaps only, the paper's measured path, A38) beside it
     gaps_ms = []
     for db, ws in zip(dbs, wss):
         gc.decode_stage(db, out, ws, False, gc.STAGE_RESET | gc.STAGE_INDEX, stream)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         gc.decode_stage(db, out, ws, False, gc.STAGE_DECODE, stream)  # (warm)
         g0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             gc.decode_stage(db, out, ws, False, gc.STAGE_DECODE, stream)
         g1.record(stream)
         torch.cuda.synchronize(dev)
-        gaps_ms.append(g0.elapsed_time(g1) / args.steps)
+        gaps_ms.append(g0.elapsed_time(g1) / steps)
 
-    # ---- NCCL: max time over ranks; sum of counts / checksums / status (after timing)
+    # ---- parity after timing: device status and the G7 checksum of every variant
     status = 0
     chk = np.zeros(3, np.uint64)
     for db, ws in zip(dbs, wss):
         docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
         status |= gc.read_device_status(ws)
-        chk += gc.checksum(db, docs, list_base=list_base).cpu().numpy().view(np.uint64)
+        chk += gc.checksum(db, docs, list_base=w.list_base).cpu().numpy().view(np.uint64)
+    peak, _ = peaks()
+    algo = [hb.compressed_bytes + 4 * hb.total_out for hb in hbs]
+    per = {}
+    for lab, hb, a, dm, im, gm in zip(labels, hbs, algo, dec_ms, idx_ms, gaps_ms):
+        per[lab] = {
+            "config": w.name, "n_ints": hb.total_out,
+            "ints_per_s": hb.total_out / ((dm + im) / 1e3),
+            "decode_kernel_ms": round(dm, 5), "index_ms": round(im, 5),
+            "bits_per_int": round(8 * hb.compressed_bytes / max(hb.total_out, 1), 3),
+            "algorithmic_bytes": a,
+            "decode_kernel_gbs": round(a / (dm / 1e3) / 1e9, 1),
+            "frac_of_peak": round(a / (dm / 1e3) / 1e9 / peak, 3),
+            "gaps_only_decode_kernel_ms": round(gm, 5),
+            "gaps_only_frac_of_peak": round(a / (gm / 1e3) / 1e9 / peak, 3),
+            "traffic": ncu_traffic(w.name, lab),
+        }
+        if flush is not None:
+            per[lab]["l2"] = "flushed before every timed step"
+    res = dict(w=w, hbs=hbs, labels=labels, per=per, algo=algo, dec_ms=dec_ms, gaps_ms=gaps_ms,
+               ms=ms, step_ms=step_ms, n_ints=n_ints, n_ints_all=sum(hb.total_out for hb in hbs),
+               verified=verified, status=status, chk=chk, small_extra=small_extra, clk=clk,
+               t_setup=t_setup, flush=flush is not None, l2_bytes=l2_bytes, algo_ws=algo_ws)
+    del dbs, wss, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    args = parse_args()
+    if maybe_spawn(args):
+        return
+    rank, local_rank, world = dist_info()
+    if args.config == 0:
+        args.config = 5 if world > 1 else 2
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.encode:
+        import torch
+        from paper_1502_01916_b200 import build
+        build.build()
+        torch.cuda.set_device(local_rank)
+        if rank == 0:
+            run_encode(args, torch.device("cuda", local_rank))
+        return
+    import torch
+    from paper_1502_01916_b200 import build
+    if local_rank == 0:
+        build.build()
+    from paper_1502_01916_b200 import gc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+        pg.barrier()  # (local rank 0 has built libgc.so)
+    else:
+        build.build()
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    codecs = config_codecs(args.config, zeta)
+    if args.codecs:
+        keep = set(args.codecs.split(","))
+        codecs = [c for c in codecs if gc.codec_label(c[0], c[1], c[2]) in keep]
+
+    w, list_base, scaling = make_workload(args, rank, world)
+    w.list_base = list_base
+    R = time_variants(args, w, codecs, dev, pg, args.steps, args.warmup, headline=True)
+    hbs, labels, algo, dec_ms = R["hbs"], R["labels"], R["algo"], R["dec_ms"]
+    ms, n_ints, n_ints_all = R["ms"], R["n_ints"], R["n_ints_all"]
+
+    # ---- the other single-GPU configs at full size, for per_codec (not in `value`)
+    extra = args.extra_configs
+    if extra == "auto":
+        extra = "1,3,4" if (world == 1 and args.config == 2 and not args.codecs
+                            and args.scale == 1.0) else "none"
+    per_codec = dict(R["per"])
+    extra_cfgs = [] if extra == "none" else [int(x) for x in extra.split(",")]
+    for k in extra_cfgs:
+        import gen
+        wk = gen.config(k)
+        wk.list_base = 0
+        Rk = time_variants(args, wk, config_codecs(k, zeta), dev, None,
+                           max(3, min(args.steps, 20)), max(3, args.warmup), headline=False)
+        per_codec.update(Rk["per"])
+        R["verified"] = None if R["verified"] is None else bool(R["verified"] and Rk["verified"])
+        R["status"] |= Rk["status"]
+        del Rk
+
+    # ---- NCCL: max time over ranks; sum of counts / checksums / status (after timing)
     from paper_1502_01916_b200 import dist as gdist
-    ms, total_ints, _, all_verified, chk = gdist.reduce_run(
-        pg, dev, ms, int(n_ints_all), status, verified, chk)
+    ms, total_ints, status, all_verified, chk = gdist.reduce_run(
+        pg, dev, ms, int(n_ints_all), R["status"], R["verified"], R["chk"])
     if rank != 0:
         if pg:
             pg.destroy_process_group()
@@ -518,24 +645,14 @@ def main():
 
     ints_per_step_all = total_ints
     value = ints_per_step_all * args.steps / (ms / 1e3)
-    # ---- roofline of the dominant kernel (k_decode, all variants): algorithmic bytes =
-    # compressed stream bytes + 4 B per decoded int; directory excluded.
-    algo = [hb.compressed_bytes + 4 * hb.total_out for hb in hbs]
+    # ---- roofline of the dominant kernel (k_decode, the headline's variants): algorithmic
+    # bytes = compressed stream bytes + 4 B per decoded int; directory excluded.
     achieved = sum(algo) / (sum(dec_ms) / 1e3) / 1e9
     peak, peak_src = peaks()
-    traffic = ncu_traffic(w.name)
-    per_codec = {}
-    for lab, hb, a, dm, im, gm in zip(labels, hbs, algo, dec_ms, idx_ms, gaps_ms):
-        per_codec[lab] = {
-            "ints_per_s": hb.total_out / ((dm + im) / 1e3),
-            "decode_kernel_ms": round(dm, 5), "index_ms": round(im, 5),
-            "bits_per_int": round(8 * hb.compressed_bytes / max(hb.total_out, 1), 3),
-            "decode_kernel_gbs": round(a / (dm / 1e3) / 1e9, 1),
-            "frac_of_peak": round(a / (dm / 1e3) / 1e9 / peak, 3),
-            "gaps_only_decode_kernel_ms": round(gm, 5),
-            "gaps_only_frac_of_peak": round(a / (gm / 1e3) / 1e9 / peak, 3),
-        }
-    gaps_achieved = sum(algo) / (sum(gaps_ms) / 1e3) / 1e9
+    gaps_achieved = sum(algo) / (sum(R["gaps_ms"]) / 1e3) / 1e9
+    tr = [per_codec[lab]["traffic"] for lab in labels]
+    traffic = (sum(t["bytes_per_launch"] for t in tr) / len(tr)
+               if tr and all(t is not None for t in tr) else None)
 
     # ---- e2e through the C ABI from pinned HOST buffers (copies inside the timed region)
     e2e = None
@@ -564,9 +681,9 @@ def main():
             host_outs.append((t, t.numpy().view(np.uint32)[:n_ints]))
             scratches.append(torch.empty(max(gc.host_scratch_size(p) for p, _ in pinned),
                                          dtype=torch.uint8, device=dev))
-        del dbs, wss, out
         torch.cuda.empty_cache()
         pipes = [torch.cuda.Stream(dev) for _ in range(n_pipe)]
+        stream = torch.cuda.current_stream(dev)
 
         def e2e_step():
             for i, (phb, _) in enumerate(pinned):
@@ -606,6 +723,8 @@ def main():
                "value_1_thread": rate1,
                "sample_1_thread": f"first {frac / 8:.4f} of the lists ({n1} ints), {reps1} rep(s)"}
 
+    step_ms = R["step_ms"]
+    l2_bytes, algo_ws = R["l2_bytes"], R["algo_ws"]
     line = {
         "metric": METRIC, "value": value, "unit": "ints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -613,10 +732,12 @@ def main():
         "data": "synthetic",
         "config": {"workload": w.name, "n_ints_per_gpu": w.n_ints, "n_lists_per_gpu": int(len(w.list_n)),
                    "codecs": labels, "ints_per_step_all_gpus": ints_per_step_all,
+                   "value_is": f"{w.name}: every variant of the config, one step = each decoded once",
+                   "per_codec_extra_configs": [f"cfg{k}" for k in extra_cfgs],
                    "parallelism": f"dp{world} (lists sharded by rank, {scaling} scaling)",
                    "l2": (f"flushed before every timed step (scratch write of {4 * l2_bytes >> 20} MB; "
                           f"working set {max(algo_ws) / 1e6:.1f} MB < the {l2_bytes >> 20} MB L2), "
-                          "steps timed without the flush" if flush is not None else
+                          "steps timed without the flush" if R["flush"] else
                           "no flush: every variant's working set "
                           f"({min(algo) / 1e6:.0f}-{max(algo) / 1e6:.0f} MB) exceeds the "
                           f"{l2_bytes >> 20} MB L2"),
@@ -628,22 +749,25 @@ def main():
                                 "serial: index then decode, variant by variant")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_decode (all variants)", "algorithmic_bytes_per_step": sum(algo),
+                     "traffic_source": ("profiles/r2_traffic.json: dram__bytes_read.sum + "
+                                        "lts__t_sectors_srcunit_tex_op_write.sum x 32 B per k_decode "
+                                        "launch, ncu --set full, mean over the headline variants"),
+                     "kernel": "k_decode (the headline's variants)", "algorithmic_bytes_per_step": sum(algo),
                      "frac_of_nominal_8tbs": achieved / 8000.0,
                      "gaps_only": {"achieved": gaps_achieved, "frac": gaps_achieved / peak,
                                    "path": "gc_decode (no d-gap scan), the paper's measured path"}},
         "step_ms": {"mean": ms / args.steps, "median": step_ms[len(step_ms) // 2],
                     "min": step_ms[0], "max": step_ms[-1]},
-        "small_workload": small_extra,
+        "small_workload": R["small_extra"],
         "per_codec": per_codec,
         "cpu_baseline": cpu,
         "e2e": e2e,
         # per variant per step: k_lists + k_index (GC_STAGE_INDEX) and k_decode (GC_STAGE_DECODE)
         "gpu_launches": 3 * len(hbs) * args.steps,
-        "clocks": clk.summary(),
+        "clocks": R["clk"].summary() if R["clk"] else None,
         "parity": {"verified": all_verified, "device_status": status,
                    "checksum": [int(x) for x in chk]},
-        "setup_s": round(t_setup, 1),
+        "setup_s": round(R["t_setup"], 1),
     }
     print(json.dumps(line), flush=True)
     if pg:

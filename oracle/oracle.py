@@ -327,15 +327,3 @@ def decode_batch(bt: dict, dgaps: bool = True, threads: int = 1, out: np.ndarray
         raise OracleError(rc, f"list {bad.value}")
     return out[:int(bt["total_out"])]
 
-
-def dgap_prefix(gaps, list_n) -> np.ndarray:
-    """Per-list inclusive prefix sum mod 2^32 (A36) of a concatenated gap array."""
-    g = np.asarray(gaps, dtype=np.uint64)
-    ln = np.asarray(list_n, dtype=np.int64)
-    if len(g) == 0:
-        return np.zeros(0, np.uint32)
-    cs = np.cumsum(g, dtype=np.uint64)                 # wraps mod 2^64; we keep mod 2^32
-    starts = np.concatenate([[0], np.cumsum(ln)[:-1]])
-    before = np.where(starts > 0, cs[np.maximum(starts - 1, 0)], np.uint64(0))
-    base = np.repeat(before.astype(np.uint64), ln)
-    return ((cs - base) & np.uint64(0xFFFFFFFF)).astype(np.uint32)

@@ -506,6 +506,17 @@ namespace {
 // Short lists (n < kVbShort, the fallback's case): one thread per list, a serial byte loop
 // (staging a warp's 32 lists in shared memory first measured slower).
 constexpr uint32_t kVbShort = 64;
+// The directory checks of k_lists for one Variable Byte list (that path runs no k_lists):
+// out_off is the exclusive scan of list_n and inside the output, the control range is
+// ordered and inside the batch.  A list that fails is flagged GC_DEV_TRUNCATED and skipped.
+__device__ __forceinline__ bool vb_list_ok(const Dev& D, uint64_t l, uint32_t n) {
+  const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1];
+  const uint64_t o0 = D.out_off[l], o1 = D.out_off[l + 1];
+  bool ok = c1 >= c0 && c1 <= 4 * D.n_ctrl_words && o1 == o0 + n && o1 <= D.total_out;
+  if (l == 0) ok = ok && o0 == 0 && c0 == 0;
+  if (l + 1 == D.n_lists) ok = ok && o1 == D.total_out;
+  return ok;
+}
 template <bool DGAPS>
 __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restrict__ out) {
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(D.ctrl_words);
@@ -513,12 +524,12 @@ __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restri
   for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < D.n_lists;
        l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t n = D.list_n[l];
-    if (n == 0 || n >= kVbShort) continue;
-    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
-    if (c1 < c0 || c1 > 4 * D.n_ctrl_words) {
+    if (!vb_list_ok(D, l, n)) {
       err |= GC_DEV_TRUNCATED;
       continue;
     }
+    if (n == 0 || n >= kVbShort) continue;
+    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
     uint64_t p = c0;
     uint32_t acc = 0;
     for (uint32_t i = 0; i < n; i++) {
@@ -560,10 +571,7 @@ __global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ o
     todo &= todo - 1;
     const uint32_t n = D.list_n[l];
     const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
-    if (c1 < c0 || c1 > 4 * D.n_ctrl_words) {
-      err |= GC_DEV_TRUNCATED;
-      continue;
-    }
+    if (!vb_list_ok(D, l, n)) continue;  // (flagged by k_varbyte_short, which checks every list)
     uint32_t got = 0, run = 0, carry = 0;  // ints so far, bytes of the open int, d-gap carry
     uint32_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;  // the previous round's last four bytes
     for (uint64_t r = c0; r < c1 && got < n; r += 32) {
@@ -612,11 +620,11 @@ __global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ o
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);
 }
 
-int num_sms();
-gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
+gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages,
+                         int n_sm) {
   if (!(stages & GC_STAGE_DECODE)) return GC_OK;
-  const uint64_t blocks = mn64((D.n_lists + 7) / 8, (uint64_t)num_sms() * 16);
-  const uint64_t sblocks = mn64((D.n_lists + 255) / 256, (uint64_t)num_sms() * 16);
+  const uint64_t blocks = mn64((D.n_lists + 7) / 8, (uint64_t)n_sm * 16);
+  const uint64_t sblocks = mn64((D.n_lists + 255) / 256, (uint64_t)n_sm * 16);
   if (dgaps) {
     k_varbyte_short<true><<<(unsigned)mx64(sblocks, 1), 256, 0, st>>>(D, out);
     k_varbyte<true><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
@@ -686,60 +694,48 @@ gc_status check_batch(const gc_batch* b, bool device_ptrs) {
   return GC_OK;
 }
 
-gc_status check_device() {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0;
-    cudaDeviceProp prop;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
-      return GC_ERR_CUDA;
-    ok = prop.major == 10 ? 1 : 0;
-  }
-  return ok ? GC_OK : GC_ERR_UNSUPPORTED_DEVICE;
-}
-
-int num_sms() {
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 148;
-  }
-  return n_sm;
+// Per-device launch facts.  Nothing is cached across calls in process-wide statics: the
+// device is the caller's current one, and the dynamic shared memory attribute (a
+// per-device property of a kernel) is set on every launch -- both cost microseconds.
+struct DevInfo {
+  int dev, n_sm;
+};
+gc_status device_info(DevInfo* di) {
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&di->n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return GC_ERR_CUDA;
+  di->dev = dev;
+  if (major != 10) return GC_ERR_UNSUPPORTED_DEVICE;
+  return di->n_sm > 0 ? GC_OK : GC_ERR_CUDA;
 }
 
 template <class C>
-gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages) {
+gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages,
+                       const DevInfo& di) {
   if (stages & GC_STAGE_INDEX) {
     const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
-    k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)num_sms() * 8), kThreads, 0, st>>>(D);
+    k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)di.n_sm * 8), kThreads, 0, st>>>(D);
     if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
     k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
     if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
   }
   if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
   const uint32_t smem = DS<C>::bytes();
-  static bool attr_set[2] = {false, false};
-  static int per_sm[2] = {0, 0};
 #ifdef GC_ABL_NODGAP
   auto kern = k_decode<C, false>;
 #else
   auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
 #endif
-  if (!attr_set[dgaps]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return GC_ERR_CUDA;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dgaps], kern, kDT, smem) !=
-            cudaSuccess ||
-        per_sm[dgaps] < 1)
-      return GC_ERR_CUDA;
-    attr_set[dgaps] = true;
-  }
+  int per_sm = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDT, smem) != cudaSuccess)
+    return GC_ERR_CUDA;
+  if (per_sm < 1) return GC_ERR_CUDA;  // (cannot happen on sm_100: the kernel fits one SM)
   // tiles are assigned round-robin to a co-resident grid (the decoupled look-back waits on
   // earlier tiles, which must all be running): a cooperative launch guarantees residency
-  const unsigned grid = (unsigned)mn64(D.tile_end - D.tile_begin, (uint64_t)num_sms() * per_sm[dgaps]);
+  const unsigned grid = (unsigned)mn64(D.tile_end - D.tile_begin, (uint64_t)di.n_sm * per_sm);
   if (grid == 0) return GC_OK;
   Dev Dv = D;
   void* args[] = {&Dv, &out};
@@ -758,7 +754,8 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
     return GC_ERR_INVALID_ARGUMENT;
   WsLayout L = ws_layout(b);
   if (ws_bytes < L.bytes) return GC_ERR_WORKSPACE_TOO_SMALL;
-  s = check_device();
+  DevInfo di;
+  s = device_info(&di);
   if (s != GC_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* w = (uint8_t*)ws;
@@ -792,31 +789,31 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
                                                : mn64((range_first + range_count + kT - 1) / kT, L.n_tiles_b));
   switch (b->codec) {
     case GC_VARBYTE:
-      return launch_varbyte(D, out, dgaps, st, stages);
+      return launch_varbyte(D, out, dgaps, st, stages, di.n_sm);
     case GC_GROUP_SIMPLE:
-      return launch_codec<CodecGS>(D, out, dgaps, st, stages);
+      return launch_codec<CodecGS>(D, out, dgaps, st, stages, di);
     case GC_GROUP_AFOR:
-      return launch_codec<CodecAFOR>(D, out, dgaps, st, stages);
+      return launch_codec<CodecAFOR>(D, out, dgaps, st, stages, di);
     case GC_GROUP_PFD:
       if (b->variant == 1)  // SIMD-BP128: no exception stream
-        return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32, false>>(D, out, dgaps, st, stages)
-                                        : launch_codec<CodecPFD<128, false>>(D, out, dgaps, st, stages);
-      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st, stages)
-                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st, stages);
+        return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32, false>>(D, out, dgaps, st, stages, di)
+                                        : launch_codec<CodecPFD<128, false>>(D, out, dgaps, st, stages, di);
+      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st, stages, di)
+                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st, stages, di);
     default:
       break;
   }
   switch (b->variant) {
-    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st, stages);
-    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st, stages);
-    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st, stages);
-    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st, stages);
-    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st, stages);
-    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st, stages);
-    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st, stages);
-    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st, stages);
-    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st, stages);
-    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st, stages);
+    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st, stages, di);
+    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st, stages, di);
+    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st, stages, di);
+    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st, stages, di);
+    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st, stages, di);
+    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st, stages, di);
+    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st, stages, di);
+    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st, stages, di);
+    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st, stages, di);
+    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st, stages, di);
     default: return GC_ERR_BAD_VARIANT;
   }
 }

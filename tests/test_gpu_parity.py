@@ -138,6 +138,11 @@ def test_malformed_streams_flagged_not_faulting():
     hb.ctrl_off[1:] = np.minimum(hb.ctrl_off[1:], hb.ctrl_off[1])  # lists 1.. have no bytes
     _, s = gpu_decode(hb, True)
     assert s & 16
+    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.VARBYTE))
+    hb.out_off = hb.out_off.copy()
+    hb.out_off[3] += 1                                        # inconsistent directory
+    _, s = gpu_decode(hb, True)
+    assert s & 16
     hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_PFD, 0))
     if hb.exc_off[-1] > 0:                                   # a PFD frame with exceptions
         hb.variant = 1                                       # read as BP128: none allowed
@@ -216,6 +221,44 @@ def test_concurrent_streams_distinct_workspaces():
         assert np.array_equal(hv, want)
 
 
+def test_concurrent_host_threads():
+    """No process-wide mutable state in the launch path (include/gc.h): four host threads,
+    each with its own stream and workspace, decode different codecs at the same time from
+    a cold start of every kernel (the shared-memory attribute and occupancy are per call)."""
+    import threading
+    rng = np.random.default_rng(12)
+    jobs = []
+    for codec, variant in [(O.GROUP_SIMPLE, 0), (O.GROUP_SCHEME, O.gsc_variant(2, "B")),
+                           (O.GROUP_PFD, 1), (O.GROUP_AFOR, 0)]:
+        w = gen.random_lists(rng, 500, 30000, 15, 0.01)
+        hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, codec, variant))
+        jobs.append((hb, O.decode_batch(hb.as_dict(), dgaps=True, threads=4)))
+    results, errors = [None] * len(jobs), []
+
+    def run(i):
+        try:
+            hb, _ = jobs[i]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                db = gc.to_device(hb)
+                for _ in range(3):
+                    out, ws = gc.decode_dgaps(db, stream=s)
+                s.synchronize()
+                results[i] = (out[:hb.total_out].cpu().numpy().view(np.uint32).copy(),
+                              gc.read_device_status(ws))
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (hb, want), (got, st) in zip(jobs, results):
+        assert st == 0
+        assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
 def test_fuzz_repeated(codec, variant):
     """Seeded random batch shapes (list-length mixes from 1-int lists to lists spanning many
@@ -268,22 +311,24 @@ def test_decode_range_random_access(codec, variant):
     the workspace's per-tile skip table and carries equal the full decode on the covering
     tiles and leave every other output position untouched (both paths)."""
     w = gen.config(2, scale=1 / 32)
-    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, codec, variant))
+    ref = O.encode_batch(w.values, w.list_n, codec, variant)
+    hb = gc.HostBatch.from_dict(ref)
     db = gc.to_device(hb)
     rng = np.random.default_rng(5)
-    T = 8192
+    T = 8192   # the decoder's CTA tile
     for dgaps in (True, False):
-        full, ws = (gc.decode_dgaps if dgaps else gc.decode)(db)
-        full = full.clone()
+        want = O.decode_batch(ref, dgaps=dgaps, threads=4).view(np.int32)   # the oracle's bytes
+        _, ws = (gc.decode_dgaps if dgaps else gc.decode)(db)
         for _ in range(6):
             first = int(rng.integers(0, hb.total_out))
             count = int(rng.integers(1, min(5 * T, hb.total_out - first) + 1))
             out = torch.full((hb.total_out,), -7, dtype=torch.int32, device="cuda")
             gc.decode_range(db, out, ws, first, count, dgaps)
             torch.cuda.synchronize()
+            got = out.cpu().numpy()
             a, b = (first // T) * T, min(hb.total_out, -(-(first + count) // T) * T)
-            assert torch.equal(out[a:b], full[a:b]), (dgaps, first, count)
-            assert bool((out[:a] == -7).all()) and bool((out[b:] == -7).all())
+            assert np.array_equal(got[a:b], want[a:b]), (dgaps, first, count)
+            assert (got[:a] == -7).all() and (got[b:] == -7).all()
         assert gc.read_device_status(ws) == 0
 
 
