@@ -254,6 +254,13 @@ gc_status gc_encode_device_write(const gc_encode_params* p, const uint32_t* valu
 const char* gc_status_string(gc_status s);
 int gc_abi_version(void);
 
+/* How this library was built (host only, no launch): GC_BUILD_CHECKED when every shared-
+ * and global-memory index of the decode kernels is asserted at run time (-DGC_CHECKED, a
+ * debugging build: a failed check prints the kernel line and traps), GC_BUILD_TIMING when
+ * the decode phases are timed into the workspace header (-DGC_TIMING).  Product builds: 0. */
+enum { GC_BUILD_CHECKED = 1, GC_BUILD_TIMING = 2 };
+int gc_build_flags(void);
+
 #ifdef __cplusplus
 }
 #endif

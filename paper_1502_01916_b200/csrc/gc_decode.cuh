@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     uint4* o4 = reinterpret_cast<uint4*>(out + tT);
 #pragma unroll 2
     for (uint32_t c = tid; c < cfast; c += kDT) {
+      GC_CHECK(tT + 4 * c + 4 <= D.total_out);
       uint4 v = s_out4[sw_chunk(kHalo / 4 + c)];
       v.x += cin;
       v.y += cin;
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
         if (p + 1 < reset0) v.y += cin;
         if (p + 2 < reset0) v.z += cin;
       }
+      GC_CHECK(tT + p + 4 <= D.total_out || p + 4 > nvalid);
       if (p + 4 <= nvalid) {
         __stcs(reinterpret_cast<uint4*>(out + tT) + c, v);
       } else {
@@ -328,9 +330,11 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       const uint32_t m = min(pos >> 5, dlim - 1u), off = pos & 31u;
       uint4 v0, v1;
       if constexpr (kStaged) {
+        GC_CHECK(m + 1 <= DS<C>::kDC);
         v0 = s_data[m];
         v1 = s_data[m + 1];  // slack vector past the staged range
       } else {
+        GC_CHECK(va + m < D.data_vectors);
         v0 = __ldg(D.data + va + m);
         v1 = __ldg(D.data + va + min(m + 1, dlim - 1u));
       }
@@ -344,6 +348,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       const uint32_t x2 = (((v0.z << shl) >> shr) & ~ml) | (v1.z & ml);
       const uint32_t x3 = (((v0.w << shl) >> shr) & ~ml) | (v1.w & ml);
       idx = min(idx, kStW - 4u);
+      GC_CHECK(sw_word(idx) < kStW && sw_word(idx + 3) < kStW);
       if (rem >= 4u && (idx & 3u) == 0) {
         s_out4[sw_chunk(idx >> 2)] = make_uint4(x0, x1, x2, x3);
       } else {
@@ -362,6 +367,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       if (lr) __syncthreads();  // the previous list round is done with the table
       if (tid < cnt) {
         const uint64_t l = la + lr + tid;
+        GC_CHECK(l < D.n_lists && tid < kLC);
         const uint32_t n = D.list_n[l];
         const uint32_t Q = (n + 3) >> 2;
         const uint32_t klo = l == la ? E0k : 0u;
@@ -423,6 +429,8 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
             const uint32_t un = my0 + k, w = un / P, part = un % P;
             while (li + 1 < cnt && lt_cw[li + 1] <= w) li++;
             wl[k] = li;
+            GC_CHECK(w >= ncw || !G.ctrl_st || w < DS<C>::kCC);
+            GC_CHECK(w >= ncw || cbase + w < D.n_ctrl_words);
             wv[k] = w < ncw ? cwp[w] : 0u;
             pv[k] = (C::kNeedsPrev && w >= 1 && w - 1 < ncw) ? cwp[w - 1] : 0u;
             const uint32_t widx = w - lt_cw[li];
@@ -479,6 +487,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
                     } else {
                       uint32_t pprev = 0;
                       for (uint32_t x = 0; x < g.cnt; x++) {
+                        GC_CHECK(e0 + x * pb + pb <= elim && (!G.exc_st || elim <= kECap));
                         uint32_t p = eptr[e0 + x * pb];
                         if (pb == 2) p |= (uint32_t)eptr[e0 + x * pb + 1] << 8;
                         if (p >= 4u * g.fq || (x > 0 && p <= pprev)) {
@@ -489,6 +498,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
                         if (p < ta) continue;
                         if (p >= tb) break;
                         const uint32_t b0 = e0 + g.cnt * pb + x * g.wb;
+                        GC_CHECK(b0 + g.wb <= elim);
                         uint32_t v = eptr[b0];
                         if (g.wb > 1) v |= (uint32_t)eptr[b0 + 1] << 8;
                         if (g.wb > 2) v |= ((uint32_t)eptr[b0 + 2] << 16) | ((uint32_t)eptr[b0 + 3] << 24);
@@ -596,7 +606,10 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     auto store_plain = [&](uint32_t c0, uint32_t c1) {  // whole chunks, no carry
       uint4* o4 = reinterpret_cast<uint4*>(out + tT);
 #pragma unroll 2
-      for (uint32_t c = c0 + tid; c < c1; c += kDT) __stcs(o4 + c, s_out4[sw_chunk(kHalo / 4 + c)]);
+      for (uint32_t c = c0 + tid; c < c1; c += kDT) {
+        GC_CHECK(tT + 4 * c + 4 <= D.total_out);
+        __stcs(o4 + c, s_out4[sw_chunk(kHalo / 4 + c)]);
+      }
     };
     if (DGAPS) {
       const uint32_t reset0 = s_reset0[buf];

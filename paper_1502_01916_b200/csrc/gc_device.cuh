@@ -111,6 +111,26 @@ __host__ __device__ __forceinline__ int64_t smin64(int64_t a, int64_t b) { retur
 __host__ __device__ __forceinline__ int64_t smax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __host__ __device__ __forceinline__ uint32_t mn32(uint32_t a, uint32_t b) { return a < b ? a : b; }
 
+// ---------------------------------------------------------------- checked builds
+// -DGC_CHECKED (the stand-in for compute-sanitizer, which this pool does not run): every
+// shared- and global-memory index of the decode kernels is asserted against the extent of
+// the buffer it addresses; a failed check prints the kernel line and traps, so the test
+// that ran it fails.  Product builds compile the checks out.
+#ifdef GC_CHECKED
+#define GC_CHECK(cond)                                                                    \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("GC_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define GC_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- memory helpers
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;

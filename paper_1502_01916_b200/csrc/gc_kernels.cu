@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   // exception range
   auto walk_word = [&](uint32_t wr, uint32_t i, uint64_t q0, uint64_t d0, uint64_t e0) {
     const uint64_t gw = w0 + wr;
+    GC_CHECK(gw < D.n_ctrl_words);
     const uint32_t w = D.ctrl_words[gw];
     const uint32_t widx = wr - cw_at(i);
     const uint32_t pv = (C::kNeedsPrev && widx > 0) ? D.ctrl_words[gw - 1] : 0u;
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
         e.wd_end = cd + a.d;
         e.we_end = ce + a.e;
         e.pad = 0;
+        GC_CHECK(t < D.n_tiles_b);
         D.entries[t] = e;
       }
     }
@@ -543,12 +545,14 @@ __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restri
           err |= GC_DEV_BAD_LD;
           break;
         }
+        GC_CHECK(p < 4 * D.n_ctrl_words);
         const uint32_t b = bytes[p++];
         v |= (b & 127u) << (7 * k);
         k++;
         if (b & 128u) break;
       }
       acc = DGAPS ? acc + v : v;
+      GC_CHECK(o0 + i < D.total_out);
       out[o0 + i] = acc;
     }
   }
@@ -603,6 +607,7 @@ __global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ o
           if (lane >= (uint32_t)o) inc += t;
         }
       }
+      GC_CHECK(!keep || o0 + idx < D.total_out);
       if (keep) out[o0 + idx] = DGAPS ? carry + inc : v;
       if (DGAPS) carry += __shfl_sync(0xffffffffu, inc, 31);
       got += __popc(stops);
@@ -823,6 +828,17 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
 extern "C" {
 
 int gc_abi_version(void) { return GC_ABI_VERSION; }
+
+int gc_build_flags(void) {
+  int f = 0;
+#ifdef GC_CHECKED
+  f |= GC_BUILD_CHECKED;
+#endif
+#ifdef GC_TIMING
+  f |= GC_BUILD_TIMING;
+#endif
+  return f;
+}
 
 const char* gc_status_string(gc_status s) {
   switch (s) {

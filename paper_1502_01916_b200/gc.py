@@ -76,6 +76,7 @@ def _lib():
                                              vp, vp, vp, u64, vp]),
             "gc_status_string": (C.c_char_p, [i32]),
             "gc_abi_version": (i32, []),
+            "gc_build_flags": (i32, []),
         }
         for name, (res, args) in sigs.items():
             f = getattr(lib, name)
@@ -86,6 +87,11 @@ def _lib():
 
 def abi_version() -> int:
     return int(_lib().gc_abi_version())
+
+
+def build_flags() -> int:
+    """1: a checked build (bounds assertions in the kernels), 2: a timing build; 0: product."""
+    return int(_lib().gc_build_flags())
 
 
 def gsc_variant(cg: int, kind: str) -> int:

@@ -6,6 +6,9 @@
 """
 import csv
 import io
+import json
+import os
+import re
 import subprocess
 import sys
 from collections import defaultdict
@@ -71,5 +74,64 @@ def full(path):
         print(f"| top stalls (warps per issue) | {s} |\n")
 
 
+def kernel_label(name: str):
+    """(variant label, d-gap path?) of a k_decode / k_index instantiation, else None."""
+    m = re.search(r"k_(decode|index)<(?:gcd::)?Codec(\w+)(?:<([^>]*)>)?(?:, (?:\(bool\))?(\d|true|false))?", name)
+    if not m:
+        return None
+    kind, codec, targs, dg = m.groups()
+    ta = [t.split(")")[-1].strip() for t in (targs or "").split(",") if t]
+    if codec.startswith("Gsc"):
+        lab = f"GSC-{ta[0]}-{codec[3:]}"
+    elif codec == "GS":
+        lab = "G-SIM"
+    elif codec == "AFOR":
+        lab = "G-AFOR"
+    else:  # PFD<F, kE>
+        base = "G-PFD" if (len(ta) < 2 or ta[1] in ("1", "true")) else "BP128"
+        lab = base if ta[0] == "32" else f"{base}-F{ta[0]}"
+    return kind, lab, dg in ("1", "true")
+
+
+def traffic(path, workload, out_json="profiles/r2_traffic.json"):
+    """Per-launch traffic of each k_decode d-gap instantiation in an ncu --set full report:
+    dram__bytes_read.sum + 32 x lts__t_sectors_srcunit_tex_op_write.sum (every byte the
+    kernel writes reaches L2; the DRAM write counter misses the tail still in L2 at the
+    kernel's end), merged into out_json under `workload`."""
+    if path.endswith(".csv.gz"):  # a raw page saved on the GPU box
+        import gzip
+        out = gzip.open(path, "rt").read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+
+    def val(d, k):
+        u = units[hdr.index(k)]
+        v = float(d[k].replace(",", ""))
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+    try:
+        with open(out_json) as f:
+            db = json.load(f)
+    except Exception:  # noqa: BLE001
+        db = {}
+    ent = db.setdefault(workload, {})
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        kl = kernel_label(d["Kernel Name"])
+        if not kl or kl[0] != "decode" or not kl[2]:
+            continue
+        rd = val(d, "dram__bytes_read.sum")
+        wr_l2 = float(d["lts__t_sectors_srcunit_tex_op_write.sum"].replace(",", "")) * 32
+        ent[kl[1]] = {"bytes_per_launch": rd + wr_l2, "dram_read": rd, "l2_write": wr_l2,
+                      "dram_write": val(d, "dram__bytes_write.sum"),
+                      "duration": f'{d["gpu__time_duration.sum"]} {units[hdr.index("gpu__time_duration.sum")]}',
+                      "report": os.path.basename(path)}
+        print(workload, kl[1], ent[kl[1]])
+    with open(out_json, "w") as f:
+        json.dump(db, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])

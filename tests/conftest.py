@@ -18,3 +18,9 @@ def oracle_lib():
     import oracle
     oracle.lib()
     return oracle
+
+
+def pytest_report_header(config):
+    """Which libgc.so the GPU tests load (GC_LIB selects e.g. the -DGC_CHECKED build)."""
+    lib = os.environ.get("GC_LIB")
+    return [f"libgc: {lib}" if lib else "libgc: the product build (paper_1502_01916_b200/libgc.so)"]

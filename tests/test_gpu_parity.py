@@ -363,3 +363,14 @@ def test_decode_range_without_full_decode_is_flagged_not_hung():
     gc.decode_range(db, out, ws, 9000, 100, dgaps=True)
     torch.cuda.synchronize()
     assert gc.read_device_status(ws) & 16
+
+
+def test_library_build_flags():
+    """GC_EXPECT_CHECKED=1 (set when the suite runs against the -DGC_CHECKED build, the
+    bounds-asserting stand-in for compute-sanitizer) proves that build is the one loaded."""
+    import os
+    flags = gc.build_flags()
+    if os.environ.get("GC_EXPECT_CHECKED") == "1":
+        assert flags & 1, "GC_LIB does not point at a -DGC_CHECKED build"
+    else:
+        assert flags in (0, 1, 2, 3)
