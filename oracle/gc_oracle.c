@@ -1081,3 +1081,162 @@ void gco_batch_free(gco_batch* b) {
   free(b->exc);
   memset(b, 0, sizeof(*b));
 }
+
+/* ------------------------------------------------------------------ */
+/* Skip pointers every 512 postings (§7.5; the entry format is   */
+/* in gc_oracle.h).  Each list is walked group by group in stream order;  */
+/* every group records the control bit that makes its owning word, its   */
+/* raw quads, data lane-bits and exception bytes.                         */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  uint64_t own_bit, q0, nq, dbits, ebytes;
+} skip_grp;
+
+/* the groups of one list (at most Q + 1 of them); returns the count or -1 */
+static int64_t walk_list_groups(const gco_params* p, uint32_t n, const uint8_t* ctrl,
+                                uint64_t ctrl_bytes, const uint8_t* exc, uint64_t exc_bytes,
+                                skip_grp* g) {
+  uint64_t Q = ceil_div(n, 4), q = 0;
+  int64_t k = 0;
+  if (p->codec == GCO_GROUP_SIMPLE) {
+    for (uint64_t s = 0; q < Q; s++) {       /* selector s: bits [4s, 4s+4), one vector */
+      if ((s >> 1) >= ctrl_bytes) return -1;
+      uint32_t SEL = (ctrl[s >> 1] >> (4 * (s & 1))) & 15;
+      if (SEL > 9) return -1;
+      g[k] = (skip_grp){4 * s, q, GS_NUM[SEL], 128, 0};
+      q += GS_NUM[SEL];
+      k++;
+    }
+  } else if (p->codec == GCO_GROUP_SCHEME) {
+    uint32_t CG = gsc_cg(p->variant), kind = gsc_kind(p->variant);
+    uint64_t bitp = 0;
+    for (uint64_t j = 0; j < Q; j++) {
+      uint32_t ld, own;
+      if (kind == 0) {
+        uint64_t byte; uint32_t sh, w16;
+        bin_field_locate(CG, j, &byte, &sh, &w16);
+        if (byte + (w16 ? 1 : 0) >= ctrl_bytes) return -1;
+        uint32_t unit = w16 ? (uint32_t)ctrl[byte] | ((uint32_t)ctrl[byte + 1] << 8) : ctrl[byte];
+        ld = (unit >> sh) & mask_bits(5 - (p->variant & 3));
+        own = (uint32_t)(8 * byte + sh);
+      } else {
+        if (kind == 2 && (bitp & 7)) {       /* incomplete unary: skip the byte's padding ones */
+          uint32_t rest = 1;
+          for (uint64_t t = bitp & 7; t < 8; t++)
+            if (ubit_get(ctrl, (bitp & ~(uint64_t)7) + t) == 0) rest = 0;
+          if (rest) bitp += 8 - (bitp & 7);
+        }
+        uint32_t ones = 0;
+        for (;;) {
+          if ((bitp >> 3) >= ctrl_bytes) return -1;
+          uint32_t bit = ubit_get(ctrl, bitp);
+          bitp++;
+          if (bit == 0) break;
+          ones++;
+        }
+        ld = ones + 1;
+        own = (uint32_t)(bitp - 1);           /* the terminating 0 */
+      }
+      uint32_t bw = gco_gsc_bw(ld, p->variant);
+      g[k] = (skip_grp){own, j, 1, bw, 0};
+      k++;
+    }
+  } else if (p->codec == GCO_GROUP_AFOR) {
+    for (uint64_t f = 0; q < Q; f++) {       /* header byte f */
+      if (f >= ctrl_bytes) return -1;
+      uint32_t h = ctrl[f], code = h & 3;
+      if (code == 3) return -1;
+      uint32_t L = 8u << code, bw = ((h >> 2) & 31) + 1;
+      g[k] = (skip_grp){8 * f, q, L, 32 * ceil_div((uint64_t)L * bw, 32), 0};
+      q += L;
+      k++;
+    }
+  } else if (p->codec == GCO_GROUP_PFD) {
+    uint32_t F = p->frame_quads, pb = pfd_pos_bytes(F);
+    for (uint64_t f = 0; q < Q; f++) {       /* 4-byte header f */
+      if (4 * f + 3 >= ctrl_bytes) return -1;
+      uint32_t b = ctrl[4 * f], wcode = ctrl[4 * f + 1];
+      uint32_t count = (uint32_t)ctrl[4 * f + 2] | ((uint32_t)ctrl[4 * f + 3] << 8);
+      uint64_t qf = Q - q < F ? Q - q : F;
+      uint32_t wbytes = wcode == 0 ? 0 : (wcode == 1 ? 1 : (wcode == 2 ? 2 : 4));
+      if (b < 1 || b > 32) return -1;
+      g[k] = (skip_grp){32 * f, q, F, 32 * ceil_div(qf * b, 32), (uint64_t)count * (pb + wbytes)};
+      q += F;
+      k++;
+    }
+  } else {
+    return -1;
+  }
+  (void)exc;
+  (void)exc_bytes;
+  return k;
+}
+
+uint64_t gco_skip_entries(const gco_batch* b) {
+  uint64_t t = 0;
+  for (uint64_t l = 0; l < b->n_lists; l++) t += ceil_div(b->list_n[l], GCO_SKIP_DIST);
+  return t;
+}
+
+int gco_build_skip(const gco_params* p, const gco_batch* b, uint64_t* skip_off,
+                   gco_skip_entry* entries) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (p->codec == GCO_VARBYTE) return GCO_ERR_CODEC;
+  uint64_t e = 0;
+  for (uint64_t l = 0; l < b->n_lists; l++) {
+    skip_off[l] = e;
+    uint32_t n = b->list_n[l];
+    if (n == 0) continue;
+    uint64_t Q = ceil_div(n, 4);
+    const uint8_t* ctrl = b->ctrl + b->ctrl_off[l];
+    uint64_t cb = b->ctrl_off[l + 1] - b->ctrl_off[l];
+    skip_grp* g = (skip_grp*)malloc((size_t)(Q + 2) * sizeof(skip_grp));
+    uint32_t* x = (uint32_t*)malloc((size_t)n * 4);
+    if (!g || !x) {
+      free(g);
+      free(x);
+      return GCO_ERR_NOMEM;
+    }
+    int64_t ng = walk_list_groups(p, n, ctrl, cb, b->exc + b->exc_off[l],
+                                  b->exc_off[l + 1] - b->exc_off[l], g);
+    rc = ng < 0 ? GCO_ERR_MALFORMED
+                : gco_decode_list(p, n, ctrl, cb, b->data + 4 * b->data_off[l],
+                                  b->data_off[l + 1] - b->data_off[l], b->exc + b->exc_off[l],
+                                  b->exc_off[l + 1] - b->exc_off[l], x);
+    if (rc) {
+      free(g);
+      free(x);
+      return rc;
+    }
+    uint32_t docid = 0;  /* running sum of the ints before the block, mod 2^32 */
+    uint64_t gi = 0, t0 = 0, cq = 0, cd = 0, ce = 0;  /* groups owned by earlier words */
+    for (uint64_t blk = 0; blk < ceil_div(n, GCO_SKIP_DIST); blk++) {
+      for (uint64_t i = blk ? GCO_SKIP_DIST * (blk - 1) : 0; i < GCO_SKIP_DIST * blk; i++)
+        docid += x[i];
+      uint64_t q0 = 128 * blk;   /* the block's first quad */
+      while (!(g[gi].q0 <= q0 && q0 < g[gi].q0 + g[gi].nq)) gi++;
+      uint64_t word = g[gi].own_bit / 32;
+      /* owners are in stream order, so the earlier words own a prefix of the groups */
+      while ((int64_t)t0 < ng && g[t0].own_bit / 32 < word) {
+        cq += g[t0].nq;
+        cd += g[t0].dbits;
+        ce += g[t0].ebytes;
+        t0++;
+      }
+      gco_skip_entry* s = &entries[e++];
+      memset(s, 0, sizeof(*s));
+      s->word = (uint32_t)word;
+      s->quads = (uint32_t)cq;
+      s->data_bits = cd;
+      s->exc_bytes = (uint32_t)ce;
+      if (p->codec == GCO_GROUP_SCHEME && gsc_kind(p->variant) == 1)  /* closed form */
+        s->data_bits = (uint64_t)gsc_cg(p->variant) * 32 * word;
+      s->docid = docid;
+    }
+    free(g);
+    free(x);
+  }
+  skip_off[b->n_lists] = e;
+  return GCO_OK;
+}

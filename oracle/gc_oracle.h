@@ -114,6 +114,25 @@ int gco_decode_batch(const gco_params* p, const gco_batch* b, int dgaps, int thr
                      uint32_t* out, uint64_t* first_bad_list);
 void gco_batch_free(gco_batch* b);
 
+/* Skip pointers (§7.5: "skip list pointers for posting blocks. The skip distance
+ * ... 512 postings"): one entry per block of 512 ints of every list -- block b covers the
+ * list's ints [512b, 512b+512) -- saying where decoding of the block starts with nothing
+ * before it.  Every group of a list is OWNED by one 32-bit control word (the word holding
+ * its descriptor: Group-Simple selector, binary LD field, AFOR / PFD frame header; the
+ * terminating 0 of a unary code).  An entry names the word owning the group of the block's
+ * first quad (quad 128b) and the list's prefixes before that word: raw quads of the groups
+ * owned by earlier words, data lane-bits (complete unary: CG x 32 x word, its closed form),
+ * exception bytes (Group-PFD), and the docID before the block (the ints [0, 512b) summed
+ * mod 2^32; 0 for block 0).  skip_off[l] = sum over lists l' < l of ceil(n_l' / 512). */
+#define GCO_SKIP_DIST 512
+typedef struct {
+  uint64_t data_bits;
+  uint32_t word, quads, exc_bytes, docid, pad[2];
+} gco_skip_entry;
+uint64_t gco_skip_entries(const gco_batch* b);  /* = skip_off[n_lists] */
+int gco_build_skip(const gco_params* p, const gco_batch* b, uint64_t* skip_off,
+                   gco_skip_entry* entries);
+
 #ifdef __cplusplus
 }
 #endif

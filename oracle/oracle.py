@@ -98,6 +98,8 @@ def lib():
             "gco_decode_batch": (C.c_int, [P(Params), P(Batch), C.c_int, C.c_int, P(C.c_uint32),
                                            P(C.c_uint64)]),
             "gco_batch_free": (None, [P(Batch)]),
+            "gco_skip_entries": (C.c_uint64, [P(Batch)]),
+            "gco_build_skip": (C.c_int, [P(Params), P(Batch), P(C.c_uint64), C.c_void_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -327,3 +329,24 @@ def decode_batch(bt: dict, dgaps: bool = True, threads: int = 1, out: np.ndarray
         raise OracleError(rc, f"list {bad.value}")
     return out[:int(bt["total_out"])]
 
+
+
+SKIP_DIST = 512
+# gco_skip_entry (gc_oracle.h): the skip pointer of one 512-int block of a list
+SKIP_DTYPE = np.dtype([("data_bits", "<u8"), ("word", "<u4"), ("quads", "<u4"),
+                       ("exc_bytes", "<u4"), ("docid", "<u4"), ("pad", "<u4", (2,))])
+
+
+def build_skip(bt: dict):
+    """Skip pointers every 512 postings (§7.5) of a packed batch: (skip_off uint64
+    [L+1], entries SKIP_DTYPE [skip_off[L]]), by gco_build_skip's group-by-group walk."""
+    p = params(bt["codec"], bt.get("variant", 0), bt.get("frame_quads", 32))
+    b, keep = _as_batch_struct(bt)
+    n_e = int(lib().gco_skip_entries(C.byref(b)))
+    off = np.zeros(len(bt["list_n"]) + 1, np.uint64)
+    ent = np.zeros(max(n_e, 1), SKIP_DTYPE)
+    rc = lib().gco_build_skip(C.byref(p), C.byref(b), _u64p(off), ent.ctypes.data)
+    del keep
+    if rc:
+        raise OracleError(rc, "gco_build_skip")
+    return off, ent[:n_e]
