@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 1
+#define GC_ABI_VERSION 2
 
 typedef enum {
   GC_OK = 0,
@@ -159,18 +159,52 @@ enum { GC_STAGE_RESET = 1, GC_STAGE_INDEX = 2, GC_STAGE_DECODE = 4, GC_STAGE_ALL
 gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream, int dgaps, int stage_mask);
 
-/* Random access (the skip pointers of P:L640 at the decoder's tile
- * granularity): decode the output ints [first, first + count) -- in whole tiles of
- * 8192 ints, so every int of the tiles covering the range is written to its usual place
- * in `out` (the full-size output buffer) and nothing else is.  `ws` must hold a complete
- * gc_decode (dgaps == 0) / gc_decode_dgaps (dgaps != 0) of the same batch: its per-tile
- * entries (control word, quad / data / exception prefixes) are the skip table and its
- * per-tile inclusive d-gap prefixes the carries, so neither the reset nor the index stage
- * runs.  A d-gap range from a workspace without a complete gc_decode_dgaps sets
- * GC_DEV_TRUNCATED and decodes nothing (it never waits).  Not for GC_VARBYTE
- * (GC_ERR_UNKNOWN_CODEC).  Asynchronous on `stream`. */
-gc_status gc_decode_range(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
-                          uint64_t first, uint64_t count, int dgaps, void* stream);
+/* ---------------------------------------------------------------------------
+ * Skip pointers and random access (§7.5: "skip list pointers for posting blocks.
+ * The skip distance ... 512 postings").
+ *
+ * One entry per block of GC_SKIP_DIST ints of every list -- block b of list l covers the
+ * list's ints [512b, 512b+512) -- saying where decoding of the block starts with nothing
+ * before it.  Every group of a list is OWNED by one 32-bit control word: the word holding
+ * its descriptor (Group-Simple selector, binary LD field, AFOR / PFD frame header) or, for
+ * a unary code, its terminating 0.  An entry names the word owning the group of the
+ * block's first quad (quad 128b, word index relative to the list's ctrl_off / 4) and the
+ * list's prefixes before that word: raw quads of the groups owned by earlier words, data
+ * lane-bits (complete unary: CG x 32 x word, its closed form), exception bytes
+ * (Group-PFD), and docid = the block's d-gap carry, the list's ints [0, 512b) summed
+ * mod 2^32 (0 for block 0).  skip_off[l] = sum over lists l' < l of ceil(n_l' / 512) is
+ * list l's first entry; skip_off[n_lists] the entry count.  The layout is byte-identical
+ * to the oracle's gco_skip_entry (the tests compare the two tables). */
+#define GC_SKIP_DIST 512
+typedef struct {
+  uint64_t data_bits;
+  uint32_t word, quads, exc_bytes, docid, pad[2];
+} gc_skip_entry; /* 32 bytes */
+
+/* An upper bound of the entry count, total_out / 512 + n_lists (host only, no launch). */
+gc_status gc_skip_capacity(const gc_batch* b, uint64_t* entries);
+
+/* Build the skip table of a batch (index-building time, not the query path):
+ *   docids   DEVICE, total_out u32: the batch's gc_decode_dgaps output (the carries);
+ *   skip_off DEVICE, n_lists + 1 u64 (written);  entries DEVICE, room for
+ *   gc_skip_capacity entries (written);  ws: a decode workspace (>= gc_workspace_size bytes).
+ * Runs the control-stream scan (subsystem (a)), which knows every control word's list
+ * prefixes, and writes an entry wherever a word owns a block's first quad.  Not for
+ * GC_VARBYTE (GC_ERR_UNKNOWN_CODEC).  Asynchronous on `stream`. */
+gc_status gc_build_skip(const gc_batch* b, const uint32_t* docids, uint64_t* skip_off,
+                        gc_skip_entry* entries, void* ws, uint64_t ws_bytes, void* stream);
+
+/* Random access: decode the output ints [first, first + count) from the skip table alone
+ * -- no full decode, no index stage, no look-back: every 512-int block overlapping the
+ * range is decoded on its own from its entry (one warp per block: the block's control
+ * words parsed from the entry's word, its quads unpacked, the d-gap scan started from the
+ * entry's docid when dgaps != 0).  Exactly out[first .. first+count) is written (`out` is
+ * the batch-sized output).  ws: >= 64 bytes of DEVICE memory for the sticky GC_DEV_* bits
+ * (reset inside the call; gc_read_device_status reads them).  Not for GC_VARBYTE.
+ * Asynchronous on `stream`. */
+gc_status gc_decode_range(const gc_batch* b, const uint64_t* skip_off,
+                          const gc_skip_entry* entries, uint32_t* out, uint64_t first,
+                          uint64_t count, int dgaps, void* ws, uint64_t ws_bytes, void* stream);
 
 /* Copy the sticky GC_DEV_* bits of a workspace to *host_bits.  Synchronises
  * `stream`.  0 means the last decode on this workspace saw a well-formed batch. */

@@ -129,12 +129,6 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t kU = UnitsPerThread<C>::v;  // parse units per thread per parse chunk
-  // a range decode reads the carries a complete d-gap decode left: without one it would
-  // wait forever on unpublished tiles -- flag it instead (the flag cannot change meanwhile)
-  if (DGAPS && D.need_ready && ld_relaxed_u32(&D.hdr->dgaps_ready) == 0) {
-    if (tid == 0 && blockIdx.x == 0) atomicOr(&D.hdr->status, (uint32_t)GC_DEV_TRUNCATED);
-    return;
-  }
   const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
   const uint64_t dend = D.data_off[D.n_lists];
   const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
@@ -142,7 +136,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   // Entries of `tile` -> s_e (one warp)
   auto load_entries = [&](uint32_t tile) {
-    if (tile < D.tile_end) {
+    if (tile < D.n_tiles_b) {
       if (lane < 16) {
         reinterpret_cast<uint32_t*>(s_e)[lane] =
             reinterpret_cast<const uint32_t*>(D.entries + tile)[lane];
@@ -162,7 +156,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     const bool last = tile + 1 == D.n_tiles_b;
     g.ok = 0;
     uint32_t cbytes = 0, xbytes = 0, dbytes = 0;
-    if (tile < D.tile_end) {
+    if (tile < D.n_tiles_b) {
       const uint64_t wa = E0.w, wb = last ? cend - 1 : E1.w;
       g.ok = (E0.valid && (last || E1.valid) && wb >= wa && wb < D.n_ctrl_words &&
               E0.l < D.n_lists && (last || (E1.l >= E0.l && E1.l < D.n_lists))) ? 1u : 0u;
@@ -274,7 +268,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
   }
-  const uint32_t first_tile = D.tile_begin + blockIdx.x;
+  const uint32_t first_tile = blockIdx.x;
   if (warp == 0) load_entries(first_tile);
   if (DGAPS) s_rst[tid] = 0u;  // kT / 32 == kDT words
   if (tid == 0) {
@@ -287,7 +281,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   uint32_t buf = 0;
   long long t_last = clock64();
-  for (uint32_t tile = first_tile; tile < D.tile_end; tile += gridDim.x, buf ^= 1u) {
+  for (uint32_t tile = first_tile; tile < D.n_tiles_b; tile += gridDim.x, buf ^= 1u) {
     GC_T(0);
     // warp 1 prefetches the next tile's entries (read after this tile's unpack)
     if (warp == 1) load_entries(tile + gridDim.x);
@@ -640,15 +634,6 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     GC_T(7);
   }
   if (DGAPS && s_pend.on) flush_pending();
-  // the last CTA of a complete d-gap decode marks the workspace's carries usable for
-  // gc_decode_range (every CTA has published all its tiles before it counts itself)
-  if (DGAPS && !D.need_ready && D.tile_begin == 0 && D.tile_end == D.n_tiles_b) {
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      if (atomicAdd(&D.hdr->counter_b, 1u) == gridDim.x - 1) st_relaxed_u32(&D.hdr->dgaps_ready, 1u);
-    }
-  }
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);
 }

@@ -100,7 +100,7 @@ struct WsHeader {
   uint32_t status;
   uint32_t counter_a;
   uint32_t counter_b;
-  uint32_t dgaps_ready;  // 1 once a complete d-gap decode ran (gc_decode_range's carries)
+  uint32_t pad0;
   uint32_t pad[12];
   unsigned long long prof[24];  // GC_TIMING builds: cycles per decode phase (debugging aid)
 };

@@ -48,8 +48,10 @@ struct Dev {
   uint64_t* tiles_b;
   Entry* entries;
   uint32_t* first_list;   // [n_tiles_a] 1 + owner list of the first word of control tile a
-  uint32_t tile_begin, tile_end;  // k_decode: the output tiles to decode (gc_decode_range)
-  uint32_t need_ready;            // a range decode: the carries must come from a full decode
+  // skip pointers (gc_build_skip: k_index writes them; gc_decode_range reads them)
+  const uint32_t* docids;         // the batch's d-gap decode (the blocks' carries)
+  uint64_t* skip_off;             // [n_lists + 1]
+  gc_skip_entry* skip;            // [skip_off[n_lists]]
 };
 
 
@@ -415,6 +417,23 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
         D.entries[t] = e;
       }
     }
+    if (D.skip && n > 0) {
+      // skip pointers (§7.5): this word owns the first quad 128b of blocks b
+      // with 128b in [cq, cq + a.q), b < ceil(n / 512)
+      const uint64_t nblk = (n + GC_SKIP_DIST - 1) / GC_SKIP_DIST;
+      for (uint64_t blk = (cq + 127) / 128; blk < nblk && 128 * blk < (uint64_t)cq + a.q; blk++) {
+        const uint64_t e = D.skip_off[l] + blk;
+        GC_CHECK(e < D.skip_off[l + 1]);
+        gc_skip_entry s;
+        s.data_bits = cd - D.data_off[l] * 32ull;
+        s.word = widx;
+        s.quads = cq;
+        s.exc_bytes = (uint32_t)(ce - (D.exc_off ? D.exc_off[l] : 0ull));
+        s.docid = blk ? D.docids[c_o + GC_SKIP_DIST * blk - 1] : 0u;
+        s.pad[0] = s.pad[1] = 0;
+        D.skip[e] = s;
+      }
+    }
     const bool last = c_cwn == wr + 1;
     const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, Q, 0u};
     if (last && (uint64_t)cq + a.q < Q) err |= GC_DEV_TRUNCATED;  // control ends before Q quads
@@ -446,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
 }
 
 #include "gc_decode.cuh"
+#include "gc_skip.cuh"
 
 // =====================================================================================
 // checksum (verification only, G7)
@@ -740,7 +760,7 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   if (per_sm < 1) return GC_ERR_CUDA;  // (cannot happen on sm_100: the kernel fits one SM)
   // tiles are assigned round-robin to a co-resident grid (the decoupled look-back waits on
   // earlier tiles, which must all be running): a cooperative launch guarantees residency
-  const unsigned grid = (unsigned)mn64(D.tile_end - D.tile_begin, (uint64_t)di.n_sm * per_sm);
+  const unsigned grid = (unsigned)mn64(D.n_tiles_b, (uint64_t)di.n_sm * per_sm);
   if (grid == 0) return GC_OK;
   Dev Dv = D;
   void* args[] = {&Dv, &out};
@@ -750,23 +770,61 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   return GC_OK;
 }
 
+// What one call does: a decode (its stages), the skip-table build, or a range decode.
+enum JobKind { JOB_DECODE, JOB_SKIP, JOB_RANGE };
+struct Job {
+  JobKind kind;
+  bool dgaps;
+  int stages;
+  uint64_t first, last;  // JOB_RANGE: output ints [first, last)
+};
+
+template <class C>
+gc_status run_codec(const Dev& D, uint32_t* out, const Job& J, cudaStream_t st, const DevInfo& di) {
+  if (J.kind == JOB_DECODE) return launch_codec<C>(D, out, J.dgaps, st, J.stages, di);
+  if (J.kind == JOB_SKIP) {
+    // the control-stream scan with skip emission: k_index knows every word's list
+    // prefixes; the entry offsets come first
+    k_skip_off<<<1, kSkipT, 0, st>>>(D);
+    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+    return launch_codec<C>(D, out, true, st, GC_STAGE_INDEX, di);
+  }
+  // JOB_RANGE: the covering entries, then one warp per 512-int block
+  unsigned long long* eb = reinterpret_cast<unsigned long long*>(D.hdr->prof);
+  k_range_bounds<<<1, 1, 0, st>>>(D, J.first, J.last, eb);
+  if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+  const uint64_t blocks = (J.last - J.first) / GC_SKIP_DIST + 2 * 32;  // (a bound of the count)
+  const unsigned grid = (unsigned)mn64((blocks + kRangeW - 1) / kRangeW + 1, (uint64_t)di.n_sm * 16);
+  if (J.dgaps) k_range<C, true><<<grid, 32 * kRangeW, 0, st>>>(D, out, J.first, J.last, eb);
+  else k_range<C, false><<<grid, 32 * kRangeW, 0, st>>>(D, out, J.first, J.last, eb);
+  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
+// (the workspace's header is all a range decode uses: status and the entry bounds)
+constexpr uint64_t kRangeWsBytes = sizeof(WsHeader);
+
 gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
-                      void* stream, bool dgaps, int stages = GC_STAGE_ALL,
-                      uint64_t range_first = 0, uint64_t range_count = ~0ull) {
+                      void* stream, const Job& J, const uint32_t* docids = nullptr,
+                      const uint64_t* skip_off_in = nullptr, uint64_t* skip_off_out = nullptr,
+                      gc_skip_entry* skip = nullptr) {
   gc_status s = check_batch(b, true);
   if (s != GC_OK) return s;
-  if (!ws || !aligned16(ws) || (b->total_out && (!out || !aligned16(out))))
+  if (!ws || !aligned16(ws) || (b->total_out && J.kind != JOB_SKIP && (!out || !aligned16(out))))
     return GC_ERR_INVALID_ARGUMENT;
   WsLayout L = ws_layout(b);
-  if (ws_bytes < L.bytes) return GC_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < (J.kind == JOB_RANGE ? kRangeWsBytes : L.bytes)) return GC_ERR_WORKSPACE_TOO_SMALL;
+  if (J.kind != JOB_DECODE && b->codec == GC_VARBYTE) return GC_ERR_UNKNOWN_CODEC;  // (no groups)
   DevInfo di;
   s = device_info(&di);
   if (s != GC_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* w = (uint8_t*)ws;
-  if ((stages & GC_STAGE_RESET) && cudaMemsetAsync(ws, 0, L.bytes, st) != cudaSuccess)
+  const uint64_t reset = J.kind == JOB_RANGE ? kRangeWsBytes : L.bytes;
+  if ((J.kind != JOB_DECODE || (J.stages & GC_STAGE_RESET)) && cudaMemsetAsync(ws, 0, reset, st) != cudaSuccess)
     return GC_ERR_CUDA;
-  if (b->n_lists == 0 || b->total_out == 0) return GC_OK;
+  if (J.kind == JOB_SKIP && b->n_lists == 0)
+    return cudaMemsetAsync(skip_off_out, 0, 8, st) == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+  if (b->n_lists == 0 || b->total_out == 0 || (J.kind == JOB_RANGE && J.last <= J.first)) return GC_OK;
   Dev D;
   D.n_lists = b->n_lists;
   D.list_n = b->list_n;
@@ -788,37 +846,35 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
   D.entries = (Entry*)(w + L.off_entries);
   D.first_list = (uint32_t*)(w + L.off_first);
-  D.need_ready = range_count != ~0ull ? 1u : 0u;
-  D.tile_begin = (uint32_t)mn64(range_first / kT, L.n_tiles_b);
-  D.tile_end = (uint32_t)(range_count == ~0ull ? L.n_tiles_b
-                                               : mn64((range_first + range_count + kT - 1) / kT, L.n_tiles_b));
+  D.docids = docids;
+  D.skip_off = J.kind == JOB_SKIP ? skip_off_out : const_cast<uint64_t*>(skip_off_in);
+  D.skip = skip;
+  if (b->codec == GC_VARBYTE) return launch_varbyte(D, out, J.dgaps, st, J.stages, di.n_sm);
   switch (b->codec) {
-    case GC_VARBYTE:
-      return launch_varbyte(D, out, dgaps, st, stages, di.n_sm);
     case GC_GROUP_SIMPLE:
-      return launch_codec<CodecGS>(D, out, dgaps, st, stages, di);
+      return run_codec<CodecGS>(D, out, J, st, di);
     case GC_GROUP_AFOR:
-      return launch_codec<CodecAFOR>(D, out, dgaps, st, stages, di);
+      return run_codec<CodecAFOR>(D, out, J, st, di);
     case GC_GROUP_PFD:
       if (b->variant == 1)  // SIMD-BP128: no exception stream
-        return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32, false>>(D, out, dgaps, st, stages, di)
-                                        : launch_codec<CodecPFD<128, false>>(D, out, dgaps, st, stages, di);
-      return b->pfd_frame_quads == 32 ? launch_codec<CodecPFD<32>>(D, out, dgaps, st, stages, di)
-                                      : launch_codec<CodecPFD<128>>(D, out, dgaps, st, stages, di);
+        return b->pfd_frame_quads == 32 ? run_codec<CodecPFD<32, false>>(D, out, J, st, di)
+                                        : run_codec<CodecPFD<128, false>>(D, out, J, st, di);
+      return b->pfd_frame_quads == 32 ? run_codec<CodecPFD<32>>(D, out, J, st, di)
+                                      : run_codec<CodecPFD<128>>(D, out, J, st, di);
     default:
       break;
   }
   switch (b->variant) {
-    case 0: return launch_codec<CodecGscB<1>>(D, out, dgaps, st, stages, di);
-    case 1: return launch_codec<CodecGscB<2>>(D, out, dgaps, st, stages, di);
-    case 2: return launch_codec<CodecGscB<4>>(D, out, dgaps, st, stages, di);
-    case 3: return launch_codec<CodecGscB<8>>(D, out, dgaps, st, stages, di);
-    case 4: return launch_codec<CodecGscCU<1>>(D, out, dgaps, st, stages, di);
-    case 5: return launch_codec<CodecGscCU<2>>(D, out, dgaps, st, stages, di);
-    case 6: return launch_codec<CodecGscCU<4>>(D, out, dgaps, st, stages, di);
-    case 7: return launch_codec<CodecGscCU<8>>(D, out, dgaps, st, stages, di);
-    case 10: return launch_codec<CodecGscIU<4>>(D, out, dgaps, st, stages, di);
-    case 11: return launch_codec<CodecGscIU<8>>(D, out, dgaps, st, stages, di);
+    case 0: return run_codec<CodecGscB<1>>(D, out, J, st, di);
+    case 1: return run_codec<CodecGscB<2>>(D, out, J, st, di);
+    case 2: return run_codec<CodecGscB<4>>(D, out, J, st, di);
+    case 3: return run_codec<CodecGscB<8>>(D, out, J, st, di);
+    case 4: return run_codec<CodecGscCU<1>>(D, out, J, st, di);
+    case 5: return run_codec<CodecGscCU<2>>(D, out, J, st, di);
+    case 6: return run_codec<CodecGscCU<4>>(D, out, J, st, di);
+    case 7: return run_codec<CodecGscCU<8>>(D, out, J, st, di);
+    case 10: return run_codec<CodecGscIU<4>>(D, out, J, st, di);
+    case 11: return run_codec<CodecGscIU<8>>(D, out, J, st, di);
     default: return GC_ERR_BAD_VARIANT;
   }
 }
@@ -862,26 +918,41 @@ gc_status gc_workspace_size(const gc_batch* b, uint64_t* bytes) {
 }
 
 gc_status gc_decode(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes, void* stream) {
-  return decode_impl(b, out, ws, ws_bytes, stream, false);
+  return decode_impl(b, out, ws, ws_bytes, stream, Job{JOB_DECODE, false, GC_STAGE_ALL, 0, 0});
 }
 
 gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream) {
-  return decode_impl(b, out, ws, ws_bytes, stream, true);
+  return decode_impl(b, out, ws, ws_bytes, stream, Job{JOB_DECODE, true, GC_STAGE_ALL, 0, 0});
 }
 
 gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream, int dgaps, int stage_mask) {
   if (stage_mask & ~GC_STAGE_ALL) return GC_ERR_INVALID_ARGUMENT;
-  return decode_impl(b, out, ws, ws_bytes, stream, dgaps != 0, stage_mask);
+  return decode_impl(b, out, ws, ws_bytes, stream, Job{JOB_DECODE, dgaps != 0, stage_mask, 0, 0});
 }
 
-gc_status gc_decode_range(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
-                          uint64_t first, uint64_t count, int dgaps, void* stream) {
-  if (b && b->codec == GC_VARBYTE) return GC_ERR_UNKNOWN_CODEC;  // (no tiles)
-  if (!b || first > b->total_out || count > b->total_out - first) return GC_ERR_INVALID_ARGUMENT;
-  if (count == 0) return GC_OK;
-  return decode_impl(b, out, ws, ws_bytes, stream, dgaps != 0, GC_STAGE_DECODE, first, count);
+gc_status gc_skip_capacity(const gc_batch* b, uint64_t* entries) {
+  if (!b || !entries) return GC_ERR_INVALID_ARGUMENT;
+  *entries = b->total_out / GC_SKIP_DIST + b->n_lists;
+  return GC_OK;
+}
+
+gc_status gc_build_skip(const gc_batch* b, const uint32_t* docids, uint64_t* skip_off,
+                        gc_skip_entry* entries, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!b || !skip_off || (b->total_out && (!docids || !entries))) return GC_ERR_INVALID_ARGUMENT;
+  return decode_impl(b, nullptr, ws, ws_bytes, stream, Job{JOB_SKIP, true, GC_STAGE_INDEX, 0, 0},
+                     docids, nullptr, skip_off, entries);
+}
+
+gc_status gc_decode_range(const gc_batch* b, const uint64_t* skip_off,
+                          const gc_skip_entry* entries, uint32_t* out, uint64_t first,
+                          uint64_t count, int dgaps, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!b || first > b->total_out || count > b->total_out - first || (count && (!skip_off || !entries)))
+    return GC_ERR_INVALID_ARGUMENT;
+  return decode_impl(b, out, ws, ws_bytes, stream,
+                     Job{JOB_RANGE, dgaps != 0, GC_STAGE_DECODE, first, first + count}, nullptr,
+                     skip_off, nullptr, const_cast<gc_skip_entry*>(entries));
 }
 
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream) {
@@ -956,7 +1027,7 @@ gc_status gc_decode_host(const gc_batch* hb, uint32_t* host_out, int dgaps, void
   p += al256(4 * hb->total_out);
   void* ws = p;
   uint64_t wsb = ws_layout(hb).bytes;
-  s = decode_impl(&d, dout, ws, wsb, stream, dgaps != 0);
+  s = decode_impl(&d, dout, ws, wsb, stream, Job{JOB_DECODE, dgaps != 0, GC_STAGE_ALL, 0, 0});
   if (s != GC_OK) return s;
   if (hb->total_out && cudaMemcpyAsync(host_out, dout, 4 * hb->total_out, cudaMemcpyDeviceToHost,
                                        st) != cudaSuccess)

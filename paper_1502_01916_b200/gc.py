@@ -60,7 +60,9 @@ def _lib():
             "gc_decode": (i32, [P(CBatch), vp, vp, u64, vp]),
             "gc_decode_dgaps": (i32, [P(CBatch), vp, vp, u64, vp]),
             "gc_decode_stage": (i32, [P(CBatch), vp, vp, u64, vp, i32, i32]),
-            "gc_decode_range": (i32, [P(CBatch), vp, vp, u64, u64, u64, i32, vp]),
+            "gc_decode_range": (i32, [P(CBatch), vp, vp, vp, u64, u64, i32, vp, u64, vp]),
+            "gc_skip_capacity": (i32, [P(CBatch), P(u64)]),
+            "gc_build_skip": (i32, [P(CBatch), vp, vp, vp, vp, u64, vp]),
             "gc_read_device_status": (i32, [vp, P(C.c_uint32), vp]),
             "gc_checksum": (i32, [P(CBatch), vp, u64, vp, vp]),
             "gc_host_scratch_size": (i32, [P(CBatch), P(u64)]),
@@ -417,15 +419,52 @@ def decode_dgaps(batch: DeviceBatch, out=None, ws=None, stream=None):
 STAGE_RESET, STAGE_INDEX, STAGE_DECODE, STAGE_ALL = 1, 2, 4, 7
 
 
-def decode_range(batch: DeviceBatch, out, ws, first: int, count: int, dgaps: bool = True,
-                 stream=None):
-    """gc_decode_range: random access -- the tiles covering output ints [first, first+count)
-    decoded into the full-size `out`, from the skip table a complete decode left in `ws`."""
+SKIP_DIST = 512
+# gc_skip_entry (include/gc.h): data_bits u64, word, quads, exc_bytes, docid, pad[2] u32
+SKIP_DTYPE = np.dtype([("data_bits", "<u8"), ("word", "<u4"), ("quads", "<u4"),
+                       ("exc_bytes", "<u4"), ("docid", "<u4"), ("pad", "<u4", (2,))])
+
+
+def build_skip(batch: DeviceBatch, docids, ws=None, stream=None):
+    """gc_build_skip: the batch's skip pointers every 512 postings (§7.5) from its
+    d-gap decode `docids` (device).  Returns (skip_off int64 [L+1], entries uint8 [cap, 32])
+    device tensors; entries[:skip_off[L]] are valid."""
+    import torch
     b = batch.cstruct()
-    st = _lib().gc_decode_range(C.byref(b), out.data_ptr(), ws.data_ptr(), ws.numel(), first,
-                                count, int(dgaps), _stream_ptr(stream))
+    cap = C.c_uint64(0)
+    _lib().gc_skip_capacity(C.byref(b), C.byref(cap))
+    dev = batch.tensors["list_n"].device
+    off = torch.empty(batch.n_lists + 1, dtype=torch.int64, device=dev)
+    ent = torch.empty((max(int(cap.value), 1), 32), dtype=torch.uint8, device=dev)
+    if ws is None:
+        ws = alloc_workspace(batch, dev)
+    st = _lib().gc_build_skip(C.byref(b), docids.data_ptr(), off.data_ptr(), ent.data_ptr(),
+                              ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+    if st:
+        raise GcError(st, "gc_build_skip")
+    return off, ent
+
+
+def skip_entries_host(skip_off, entries) -> np.ndarray:
+    """The valid entries of a device skip table as a SKIP_DTYPE array (for comparisons)."""
+    n = int(skip_off[-1].item())
+    return entries[:n].cpu().numpy().reshape(-1).view(SKIP_DTYPE)
+
+
+def decode_range(batch: DeviceBatch, skip_off, entries, out, first: int, count: int,
+                 dgaps: bool = True, ws=None, stream=None):
+    """gc_decode_range: random access -- exactly out[first:first+count] decoded from the
+    skip table alone (one warp per overlapping 512-int block).  Returns the status ws."""
+    import torch
+    b = batch.cstruct()
+    if ws is None:
+        ws = torch.empty(256, dtype=torch.uint8, device=out.device)
+    st = _lib().gc_decode_range(C.byref(b), skip_off.data_ptr(), entries.data_ptr(),
+                                out.data_ptr(), first, count, int(dgaps), ws.data_ptr(),
+                                ws.numel(), _stream_ptr(stream))
     if st:
         raise GcError(st, "gc_decode_range")
+    return ws
 
 
 def decode_stage(batch: DeviceBatch, out, ws, dgaps: bool, stages: int, stream=None):

@@ -36,7 +36,7 @@ def main():
             ref = O.encode_batch(w.values, w.list_n, codec, variant)
             hb = gc.HostBatch.from_dict(ref)
             db = gc.to_device(hb)
-            for dgaps in (False, True):
+            for dgaps in (True, False):
                 out, ws = (gc.decode_dgaps if dgaps else gc.decode)(db)
                 torch.cuda.synchronize()
                 want = O.decode_batch(ref, dgaps=dgaps)
@@ -44,9 +44,14 @@ def main():
                 assert gc.read_device_status(ws) == 0 and np.array_equal(got, want), (codec, variant)
                 n_checked += 1
                 if codec != O.VARBYTE and hb.total_out > 10:
+                    if dgaps:  # the skip table from this d-gap decode, then a range from it
+                        off, ent = gc.build_skip(db, out)
                     r = torch.full((hb.total_out,), -1, dtype=torch.int32, device="cuda")
-                    gc.decode_range(db, r, ws, 5, hb.total_out // 2, dgaps)
+                    rws = gc.decode_range(db, off, ent, r, 5, hb.total_out // 2, dgaps)
                     torch.cuda.synchronize()
+                    assert gc.read_device_status(rws) == 0
+                    assert np.array_equal(r[5:5 + hb.total_out // 2].cpu().numpy().view(np.uint32),
+                                          want[5:5 + hb.total_out // 2])
         # a malformed stream: status bits, no fault
         hb = gc.HostBatch.from_dict(O.encode_batch(shapes[0].values, shapes[0].list_n, codec, variant))
         hb.ctrl = hb.ctrl.copy()

@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol():
     lib = ctypes.CDLL(gc.LIB_PATH)
     missing = [s for s in declared if not hasattr(lib, s)]
     assert declared and not missing, missing
-    assert gc.abi_version() == 1
+    assert gc.abi_version() == 2
 
 
 def _same(a: dict, b: gc.HostBatch):

@@ -304,32 +304,75 @@ def test_posting_store(codec, variant):
         assert np.array_equal(got[o:o + n], w.values[starts[i]:starts[i] + n]), i
 
 
+SKIP_CODECS = [c for c in CODECS if c[0] != O.VARBYTE]
+
+
+@pytest.mark.parametrize("codec,variant", SKIP_CODECS, ids=[gc.codec_label(c, v) for c, v in SKIP_CODECS])
+def test_build_skip_equals_oracle(codec, variant):
+    """gc_build_skip (the control scan writing an entry wherever a word owns a block's first
+    quad, §7.5) is byte-identical to the oracle's skip table, on ragged lists incl.
+    empty ones and lists of 511 / 512 / 513 ints."""
+    rng = np.random.default_rng(300 + 16 * codec + variant)
+    w = gen.random_lists(rng, 60, 9000, 16, 0.02)
+    ln = np.concatenate([w.list_n, np.array([0, 511, 512, 513, 3, 0, 1025], np.uint32)])
+    vals = np.concatenate([w.values, rng.integers(0, 1 << 18, int(ln[len(w.list_n):].sum())).astype(np.uint32)])
+    ref = O.encode_batch(vals, ln, codec, variant)
+    off_o, ent_o = O.build_skip(ref)
+    db = gc.to_device(gc.HostBatch.from_dict(ref))
+    docs, ws = gc.decode_dgaps(db)
+    off, ent = gc.build_skip(db, docs)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) == 0
+    assert np.array_equal(off.cpu().numpy().view(np.uint64), off_o)
+    assert gc.skip_entries_host(off, ent).tobytes() == ent_o.tobytes()
+
+
 @pytest.mark.parametrize("codec,variant", [(O.GROUP_SCHEME, O.gsc_variant(1, "CU")), (O.GROUP_PFD, 0),
-                                           (O.GROUP_AFOR, 0), (O.GROUP_SIMPLE, 0)])
-def test_decode_range_random_access(codec, variant):
-    """gc_decode_range (§8(f) rank 4): after one complete decode, random ranges decoded from
-    the workspace's per-tile skip table and carries equal the full decode on the covering
-    tiles and leave every other output position untouched (both paths)."""
+                                           (O.GROUP_AFOR, 0), (O.GROUP_SIMPLE, 0),
+                                           (O.GROUP_SCHEME, O.gsc_variant(8, "IU")),
+                                           (O.GROUP_SCHEME, O.gsc_variant(2, "B")), (O.GROUP_PFD, 1)])
+def test_decode_range_from_skip_table(codec, variant):
+    """gc_decode_range (§8(f) rank 4): random ranges decoded from the ORACLE's skip table alone
+    -- a fresh workspace, no full decode before -- equal the oracle's decode on exactly the
+    range, and nothing outside it is written (both paths)."""
     w = gen.config(2, scale=1 / 32)
     ref = O.encode_batch(w.values, w.list_n, codec, variant)
-    hb = gc.HostBatch.from_dict(ref)
-    db = gc.to_device(hb)
+    off_o, ent_o = O.build_skip(ref)
+    db = gc.to_device(gc.HostBatch.from_dict(ref))
+    off = torch.from_numpy(off_o.view(np.int64)).cuda()
+    ent = torch.from_numpy(ent_o.view(np.uint8).reshape(-1, 32).copy()).cuda()
     rng = np.random.default_rng(5)
-    T = 8192   # the decoder's CTA tile
+    N = int(ref["total_out"])
     for dgaps in (True, False):
-        want = O.decode_batch(ref, dgaps=dgaps, threads=4).view(np.int32)   # the oracle's bytes
-        _, ws = (gc.decode_dgaps if dgaps else gc.decode)(db)
-        for _ in range(6):
-            first = int(rng.integers(0, hb.total_out))
-            count = int(rng.integers(1, min(5 * T, hb.total_out - first) + 1))
-            out = torch.full((hb.total_out,), -7, dtype=torch.int32, device="cuda")
-            gc.decode_range(db, out, ws, first, count, dgaps)
+        want = O.decode_batch(ref, dgaps=dgaps, threads=4).view(np.int32)
+        ranges = [(0, N), (0, 1), (N - 1, 1), (511, 2), (512 * 7, 512)]
+        ranges += [(int(f), int(rng.integers(1, min(40000, N - int(f)) + 1)))
+                   for f in rng.integers(0, N - 1, 8)]
+        for first, count in ranges:
+            out = torch.full((N,), -7, dtype=torch.int32, device="cuda")
+            ws = gc.decode_range(db, off, ent, out, first, count, dgaps)
             torch.cuda.synchronize()
+            assert gc.read_device_status(ws) == 0
             got = out.cpu().numpy()
-            a, b = (first // T) * T, min(hb.total_out, -(-(first + count) // T) * T)
-            assert np.array_equal(got[a:b], want[a:b]), (dgaps, first, count)
-            assert (got[:a] == -7).all() and (got[b:] == -7).all()
-        assert gc.read_device_status(ws) == 0
+            assert np.array_equal(got[first:first + count], want[first:first + count]), (dgaps, first, count)
+            assert (got[:first] == -7).all() and (got[first + count:] == -7).all()
+
+
+def test_decode_range_flags_a_bad_table():
+    """A skip table whose entry points past its list's control sets GC_DEV_TRUNCATED and
+    writes nothing wrong outside the range (no fault)."""
+    w = gen.config(2, scale=1 / 64)
+    ref = O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME, O.gsc_variant(4, "B"))
+    off_o, ent_o = O.build_skip(ref)
+    bad = ent_o.copy()
+    bad["word"] += 1 << 20
+    db = gc.to_device(gc.HostBatch.from_dict(ref))
+    out = torch.zeros(int(ref["total_out"]), dtype=torch.int32, device="cuda")
+    ws = gc.decode_range(db, torch.from_numpy(off_o.view(np.int64)).cuda(),
+                         torch.from_numpy(bad.view(np.uint8).reshape(-1, 32).copy()).cuda(),
+                         out, 100, 5000, True)
+    torch.cuda.synchronize()
+    assert gc.read_device_status(ws) & 16
 
 
 def test_posting_store_with_term_frequencies():
@@ -350,19 +393,6 @@ def test_posting_store_with_term_frequencies():
         o, n = int(st.list_out_off[i]), int(w.list_n[i])
         assert np.array_equal(d[o:o + n], w.values[starts[i]:starts[i] + n]), i
         assert np.array_equal(t[o:o + n], tfs[starts[i]:starts[i] + n]), i
-
-
-def test_decode_range_without_full_decode_is_flagged_not_hung():
-    """A d-gap range decode from a workspace that never held a complete d-gap decode has no
-    carries: it must flag the workspace (GC_DEV_TRUNCATED) and return, not wait."""
-    w = gen.config(2, scale=1 / 64)
-    hb = gc.HostBatch.from_dict(O.encode_batch(w.values, w.list_n, O.GROUP_SCHEME, 0))
-    db = gc.to_device(hb)
-    _, ws = gc.decode(db)                    # gaps only: no carries published
-    out = torch.zeros(hb.total_out, dtype=torch.int32, device="cuda")
-    gc.decode_range(db, out, ws, 9000, 100, dgaps=True)
-    torch.cuda.synchronize()
-    assert gc.read_device_status(ws) & 16
 
 
 def test_library_build_flags():

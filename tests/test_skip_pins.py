@@ -37,7 +37,7 @@ def resume_block(codec, variant, F, n, ctrl, data, exc, ent, blk):
         if qa <= j < qb:
             got[j] = vals
     if codec == O.GROUP_SIMPLE:
-        assert dpos == 128 * 8 * w                  # one vector per selector
+        assert dpos == 32 * 8 * w                   # one vector (32 lane-bits) per selector
         s = 8 * w                                   # 8 nibbles per word; one vector each
         while q < qb:
             sel = (int(ctrl[s // 2]) >> (0 if s % 2 == 0 else 4)) & 15
