@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--random-access", action="store_true",
+                    help="time gc_decode_range from the skip table (P:L640): whole-batch and "
+                         "single-block ranges")
     return ap.parse_args()
 
 
@@ -568,6 +571,77 @@ def time_variants(args, w, codecs, dev, pg, steps, warmup, headline):
     return res
 
 
+def run_random_access(args, dev):
+    """--random-access: gc_decode_range from the skip pointers (§7.5, SURVEY §8(f)
+    rank 4) on the headline config's variants: (a) the whole batch as one range -- every
+    512-int block decoded on its own from its entry, no index stage, no look-back -- with its
+    roofline (compressed + skip-table bytes read, 4 B per int written); (b) single 512-int
+    block ranges at random positions, one call each: microseconds per call."""
+    import torch
+    from paper_1502_01916_b200 import gc
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    w, _, _ = make_workload(args, 0, 1)
+    peak, peak_src = peaks()
+    per, tot_b, tot_ms, tot_n = {}, 0, 0.0, 0
+    stream = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(11)
+    for c, v, f, z in config_codecs(args.config, zeta):
+        if c == gc.VARBYTE:
+            continue
+        lab = gc.codec_label(c, v, f)
+        hb = gc.encode_batch(*codec_subset(w, c), c, v, delta=w.delta, frame_quads=f, zeta=z)
+        db = gc.to_device(hb, dev)
+        docs, ws = gc.decode_dgaps(db)
+        want = docs.clone()
+        off, ent = gc.build_skip(db, docs, ws=ws)
+        n_ent = int(off[-1].item())
+        out = torch.empty_like(docs)
+        rws = torch.empty(256, dtype=torch.uint8, device=dev)
+        N = hb.total_out
+        for _ in range(args.warmup):
+            gc.decode_range(db, off, ent, out, 0, N, True, ws=rws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            gc.decode_range(db, off, ent, out, 0, N, True, ws=rws)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / args.steps
+        ok = bool(torch.equal(out, want)) and gc.read_device_status(rws) == 0
+        algo = hb.compressed_bytes + 4 * N + 32 * n_ent
+        # single blocks: 200 random 512-int ranges, one call each
+        firsts = rng.integers(0, max(1, N - 512), 200)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for fi in firsts:
+            gc.decode_range(db, off, ent, out, int(fi), min(512, N - int(fi)), True, ws=rws)
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        us_block = 1e3 * b0.elapsed_time(b1) / len(firsts)
+        per[lab] = {"whole_batch_ms": round(ms, 5), "ints_per_s": N / (ms / 1e3),
+                    "gbs": round(algo / (ms / 1e3) / 1e9, 1),
+                    "frac_of_peak": round(algo / (ms / 1e3) / 1e9 / peak, 3),
+                    "skip_entries": n_ent, "skip_bytes_per_int": round(32 * n_ent / max(N, 1), 4),
+                    "one_block_us_per_call": round(us_block, 2), "verified": ok}
+        tot_b += algo
+        tot_ms += ms
+        tot_n += N
+        del db, docs, want, out, off, ent, ws
+        torch.cuda.empty_cache()
+    achieved = tot_b / (tot_ms / 1e3) / 1e9
+    line = {"metric": "decoded uint32 ints/sec from the skip pointers (gc_decode_range)",
+            "value": tot_n / (tot_ms / 1e3), "unit": "ints/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms, "higher_is_better": True,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": w.name, "codecs": list(per),
+                       "path": "gc_decode_range(0, N) per variant: one warp per 512-int block"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src, "kernel": "k_range",
+                         "bytes": "compressed streams + 32 B per skip entry read, 4 B per int written"},
+            "per_codec": per}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     if maybe_spawn(args):
@@ -578,13 +652,13 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.encode:
+    if args.encode or args.random_access:
         import torch
         from paper_1502_01916_b200 import build
         build.build()
         torch.cuda.set_device(local_rank)
         if rank == 0:
-            run_encode(args, torch.device("cuda", local_rank))
+            (run_encode if args.encode else run_random_access)(args, torch.device("cuda", local_rank))
         return
     import torch
     from paper_1502_01916_b200 import build
