@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--spawn-check", action="store_true",
+                    help="(tests) start --gpus ranks, all-reduce their ranks, print one line")
     ap.add_argument("--random-access", action="store_true",
                     help="time gc_decode_range from the skip table (P:L640): whole-batch and "
                          "single-block ranges")
@@ -110,6 +112,13 @@ def codec_subset(w, codec: int):
     from paper_1502_01916_b200 import gc
     if codec != gc.VARBYTE:
         return w.values, w.list_n
+    if not isinstance(w.values, np.ndarray):  # a device-resident workload
+        import torch
+        ln = torch.from_numpy(w.list_n.astype(np.int64)).to(w.values.device)
+        short = ln < 64
+        starts = torch.cumsum(ln, 0) - ln
+        owner = torch.repeat_interleave(short, ln)
+        return w.values[owner], w.list_n[short.cpu().numpy()]
     ln = w.list_n.astype(np.int64)
     st = np.concatenate([[0], np.cumsum(ln)[:-1]]) if len(ln) else np.zeros(0, np.int64)
     ids = np.nonzero(w.list_n < 64)[0]
@@ -118,8 +127,19 @@ def codec_subset(w, codec: int):
     return vals, w.list_n[ids]
 
 
-def make_workload(args, rank, world):
-    """(workload, global id of its first list, scaling) of this rank (dist.shard_for_rank)."""
+def make_workload(args, rank, world, device=None):
+    """(workload, global id of its first list, scaling) of this rank (dist.shard_for_rank).
+    Config 5's shards (2^31 docIDs each at full size) are drawn on the rank's GPU by
+    gen.gpu -- the same counter-based draws as gen/, bit for bit -- when `device` is given:
+    then `values` is a device tensor."""
+    if device is not None and args.config == 5 and not args.strong:
+        import gen
+        from gen import gpu as G
+        shard = rank % 8
+        ln, vals, base = G.config5_shard_gpu(shard, 8, args.scale, device)
+        w = gen.Workload("cfg5_all", ln, vals, True, 4,
+                         f"config 5 shard {shard} of 8, drawn on the GPU (gen.gpu)")
+        return w, base, "weak"
     from paper_1502_01916_b200 import dist
     sh = dist.shard_for_rank(args.config, args.scale, rank, world, strong=args.strong)
     return sh.workload, sh.list_base, sh.scaling
@@ -371,6 +391,34 @@ def maybe_spawn(args):
     return True
 
 
+def oracle_slice_check(db, docs, list_n, seed: int, frac: float = 0.01) -> bool:
+    """A contiguous run of about `frac` of a device batch's ints, copied to the host with
+    its directory rebased, decoded by the oracle (d-gaps) and compared with `docs`."""
+    import oracle as O
+    L = len(list_n)
+    if L == 0:
+        return True
+    t = db.tensors
+    ln = np.asarray(list_n, np.int64)
+    cs = np.cumsum(ln)
+    rng = np.random.default_rng(seed)
+    a = int(rng.integers(0, L))
+    b = int(min(L, np.searchsorted(cs, cs[a] - ln[a] + max(1, int(frac * cs[-1])), side="right") + 1))
+    b = max(b, a + 1)
+    offs = {k: t[k][a:b + 1].cpu().numpy().view(np.uint64) for k in ("ctrl_off", "data_off", "exc_off", "out_off")}
+    sub = {"codec": db.codec, "variant": db.variant, "frame_quads": db.frame_quads,
+           "list_n": ln[a:b].astype(np.uint32),
+           "ctrl": t["ctrl"][int(offs["ctrl_off"][0]):int(offs["ctrl_off"][-1])].cpu().numpy(),
+           "data": t["data"].view(-1, 4)[int(offs["data_off"][0]):int(offs["data_off"][-1])].cpu().numpy().view(np.uint32),
+           "exc": t["exc"][int(offs["exc_off"][0]):int(offs["exc_off"][-1])].cpu().numpy()}
+    for k, v in offs.items():
+        sub[k] = v - v[0]
+    sub["total_out"] = int(sub["out_off"][-1])
+    want = O.decode_batch(sub, dgaps=True, threads=len(os.sched_getaffinity(0)))
+    got = docs[int(offs["out_off"][0]):int(offs["out_off"][-1])].cpu().numpy().view(np.uint32)
+    return bool(np.array_equal(got, want))
+
+
 def time_variants(args, w, codecs, dev, pg, steps, warmup, headline):
     """Encode (host encoder), upload, verify and time every variant of one workload.
     Returns a dict with the per-variant timings and, for the headline, the step timing."""
@@ -378,9 +426,18 @@ def time_variants(args, w, codecs, dev, pg, steps, warmup, headline):
     from paper_1502_01916_b200 import gc
     t_setup = time.perf_counter()
     subs = [codec_subset(w, c) for c, _, _, _ in codecs]
-    hbs = [gc.encode_batch(sv, sl, c, v, delta=w.delta, frame_quads=f, zeta=z)
-           for (sv, sl), (c, v, f, z) in zip(subs, codecs)]
-    dbs = [gc.to_device(hb, dev) for hb in hbs]
+    on_dev = not isinstance(w.values, np.ndarray)
+    if on_dev:  # GPU encoders (gc_encode_device_*), byte-identical to the host encoder
+        dbs = []
+        for (sv, sl), (c, v, f, z) in zip(subs, codecs):
+            lt = torch.from_numpy(np.ascontiguousarray(sl).view(np.int32)).to(dev)
+            dbs.append(gc.encode_device(sv, lt, c, v, delta=w.delta, frame_quads=f, zeta=z))
+            torch.cuda.synchronize(dev)
+        hbs = dbs
+    else:
+        hbs = [gc.encode_batch(sv, sl, c, v, delta=w.delta, frame_quads=f, zeta=z)
+               for (sv, sl), (c, v, f, z) in zip(subs, codecs)]
+        dbs = [gc.to_device(hb, dev) for hb in hbs]
     n_ints = max(hb.total_out for hb in hbs)
     out = torch.empty(max(n_ints, 4), dtype=torch.int32, device=dev)
     wss = [gc.alloc_workspace(db, dev) for db in dbs]
@@ -392,23 +449,34 @@ def time_variants(args, w, codecs, dev, pg, steps, warmup, headline):
     if not args.no_verify:
         verified = True
         for lab, db, ws, (sv, sl) in zip(labels, dbs, wss, subs):
-            vals = torch.from_numpy(np.ascontiguousarray(sv).view(np.int32)).to(dev)
+            vals = sv if on_dev else torch.from_numpy(np.ascontiguousarray(sv).view(np.int32)).to(dev)
             ln = torch.from_numpy(sl.astype(np.int64)).to(dev)
             starts = torch.cumsum(ln, 0) - ln
             starts = starts[ln > 0]
-            gaps, _ = gc.decode(db, out=out, ws=ws)
-            ok_g = bool(torch.equal(gaps, vals)) if not w.delta else None
+            if not w.delta:
+                gaps, _ = gc.decode(db, out=out, ws=ws)
+                ok_g = bool(torch.equal(gaps, vals))
+            else:
+                ok_g = None
             docs, _ = gc.decode_dgaps(db, out=out, ws=ws)
             st = gc.read_device_status(ws)
-            g = docs.clone()
-            g[1:] = docs[1:] - docs[:-1]
-            g[starts] = docs[starts]
-            ok = bool(torch.equal(docs, vals)) if w.delta else bool(torch.equal(g, vals))
+            if w.delta:
+                ok = bool(torch.equal(docs, vals))
+            else:
+                g = docs.clone()
+                g[1:] = docs[1:] - docs[:-1]
+                g[starts] = docs[starts]
+                ok = bool(torch.equal(g, vals))
+                del g
+            if ok and on_dev:
+                # the oracle decodes ~1% of the lists (a contiguous run from a seeded start)
+                # from the GPU encoder's bytes; its docIDs must equal the GPU's
+                ok = oracle_slice_check(db, docs, sl, seed=len(sl))
             if ok_g is False or not ok or st:
                 verified = False
                 print(f"PARITY FAILURE {w.name} {lab}: gaps={ok_g} docs={ok} status="
                       f"{gc.status_names(st)}", file=sys.stderr)
-            del vals, g
+            del vals
     t_setup = time.perf_counter() - t_setup
 
     # ---- timed region: K steps x all variants of gc_decode_dgaps (stage events per launch)
@@ -642,11 +710,33 @@ def run_random_access(args, dev):
     print(json.dumps(line), flush=True)
 
 
+def spawn_check(rank, world):
+    """--spawn-check: the rank plumbing alone (gloo on CPU, NCCL on GPUs): every rank
+    all-reduces its rank id; rank 0 prints {"world", "rank_sum"}."""
+    import torch
+    import torch.distributed as dist
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if backend == "nccl" else None
+    if dev is not None:
+        torch.cuda.set_device(dev)
+    dist.init_process_group(backend)
+    t = torch.tensor([rank], dtype=torch.int64, device=dev)
+    dist.all_reduce(t)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"spawn_check": True, "world": world, "rank_sum": int(t.item()),
+                          "backend": backend}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     if maybe_spawn(args):
         return
     rank, local_rank, world = dist_info()
+    if args.spawn_check:
+        spawn_check(rank, world)
+        return
     if args.config == 0:
         args.config = 5 if world > 1 else 2
     if args.impl == "reference":
@@ -684,7 +774,7 @@ def main():
         keep = set(args.codecs.split(","))
         codecs = [c for c in codecs if gc.codec_label(c[0], c[1], c[2]) in keep]
 
-    w, list_base, scaling = make_workload(args, rank, world)
+    w, list_base, scaling = make_workload(args, rank, world, device=dev)
     w.list_base = list_base
     R = time_variants(args, w, codecs, dev, pg, args.steps, args.warmup, headline=True)
     hbs, labels, algo, dec_ms = R["hbs"], R["labels"], R["algo"], R["dec_ms"]
@@ -728,6 +818,22 @@ def main():
     traffic = (sum(t["bytes_per_launch"] for t in tr) / len(tr)
                if tr and all(t is not None for t in tr) else None)
 
+    # a device-resident workload (config 5 drawn on the GPU) times e2e and the CPU baseline
+    # on host batches of its first lists (the host encoder), labelled as a sample
+    host_sample = None
+    if not isinstance(w.values, np.ndarray) and not (args.no_e2e and args.no_cpu_baseline):
+        ln64 = w.list_n.astype(np.int64)
+        nl = max(1, int(np.searchsorted(np.cumsum(ln64), 1 << 24)))
+        ns = int(ln64[:nl].sum())
+        hv = w.values[:ns].cpu().numpy().view(np.uint32)
+
+        class _W:
+            values, list_n, delta = hv, w.list_n[:nl], w.delta
+        hbs = [gc.encode_batch(*codec_subset(_W, c), c, v, delta=w.delta, frame_quads=f, zeta=z)
+               for c, v, f, z in codecs]
+        n_ints = max(hb.total_out for hb in hbs)
+        n_ints_all = sum(hb.total_out for hb in hbs)
+        host_sample = f"the shard's first {nl} lists ({ns} ints), host-encoded"
     # ---- e2e through the C ABI from pinned HOST buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -781,6 +887,8 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * n_ints_all),
                "steps": args.e2e_steps, "ms_per_step": ems / args.e2e_steps,
                "api": "gc_decode_host (pinned host buffers, batches alternating over 2 streams)"}
+        if host_sample:
+            e2e["sample"] = host_sample
 
     cpu = None
     if not args.no_cpu_baseline:

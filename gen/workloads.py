@@ -58,7 +58,8 @@ def geometric(u: np.ndarray, p: float) -> np.ndarray:
     return np.minimum(g, 2.0 ** 32 - 1).astype(np.uint64)
 
 
-def zipf_lengths(n_lists: int, total: int, s: float, lo: int, hi: int, seed: int) -> np.ndarray:
+def zipf_lengths(n_lists: int, total: int, s: float, lo: int, hi: int, seed: int,
+                 use_torch: bool = True) -> np.ndarray:
     """G2: rank-frequency Zipf lengths summing exactly to `total`, in seeded random order."""
     r = np.arange(1, n_lists + 1, dtype=np.float64)
     w = r ** (-s)
@@ -69,9 +70,21 @@ def zipf_lengths(n_lists: int, total: int, s: float, lo: int, hi: int, seed: int
     if lengths(0.0).sum() > total or lengths(1e30).sum() < total:
         raise ValueError("infeasible Zipf configuration")
     a, b = 0.0, float(hi) / w[-1] * 4 + 1.0
+    total_of = lambda C: int(lengths(C).sum())  # noqa: E731
+    if use_torch and n_lists > (1 << 20):
+        # the same IEEE float64 multiply / floor / clip and an exact int64 sum, on torch's
+        # threads (or the GPU): bit-identical lengths, minutes faster for config 5's 5e7
+        try:
+            import torch
+            wt = torch.from_numpy(w)
+            if torch.cuda.is_available():
+                wt = wt.cuda()
+            total_of = lambda C: int(torch.clamp(torch.floor(C * wt), lo, hi).to(torch.int64).sum())  # noqa: E731
+        except ImportError:
+            pass
     for _ in range(200):
         m = 0.5 * (a + b)
-        if lengths(m).sum() <= total:
+        if total_of(m) <= total:
             a = m
         else:
             b = m
@@ -173,7 +186,8 @@ class Workload:
 
     @property
     def n_ints(self) -> int:
-        return int(self.values.size)
+        v = self.values  # numpy, or a torch tensor (gen.gpu's device-resident draws)
+        return int(v.numel()) if hasattr(v, "numel") else int(v.size)
 
 
 def _gaps_cfg2(list_n, seed, base=0):

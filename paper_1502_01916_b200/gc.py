@@ -190,6 +190,18 @@ class DeviceBatch:
     data_vectors: int
     exc_bytes: int
 
+    @property
+    def compressed_bytes(self) -> int:
+        """Stream bytes (ctrl + data + exc, logical extents; reads the offsets' last entries)."""
+        L = self.n_lists
+        t = self.tensors
+        return (int(t["ctrl_off"][L].item()) + 16 * int(t["data_off"][L].item())
+                + int(t["exc_off"][L].item()))
+
+    @property
+    def directory_bytes(self) -> int:
+        return 4 * self.n_lists + 4 * 8 * (self.n_lists + 1)
+
     def cstruct(self) -> CBatch:
         t = self.tensors
 

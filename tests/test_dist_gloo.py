@@ -105,3 +105,19 @@ def test_two_ranks_gloo_reduce(tmp_path, config, scale):
                                               O.gsc_variant(8, "IU")), dgaps=True)
         want += np.array(gen.checksum(s.workload.list_n, d, s.list_base), np.uint64)
     assert r["chk"] == [int(x) for x in want]
+
+
+def test_bench_gpus_flag_starts_its_own_ranks():
+    """`python bench.py --gpus N` outside torchrun starts N ranks itself (torch.distributed.run,
+    127.0.0.1 rendezvous): here 2 gloo ranks on CPU, each all-reducing its rank id."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--spawn-check"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["world"] == 2 and d["rank_sum"] == 1
