@@ -1103,7 +1103,7 @@ static int64_t walk_list_groups(const gco_params* p, uint32_t n, const uint8_t* 
       if ((s >> 1) >= ctrl_bytes) return -1;
       uint32_t SEL = (ctrl[s >> 1] >> (4 * (s & 1))) & 15;
       if (SEL > 9) return -1;
-      g[k] = (skip_grp){4 * s, q, GS_NUM[SEL], 128, 0};
+      g[k] = (skip_grp){4 * s, q, GS_NUM[SEL], 32, 0};  /* one vector: 32 lane-bits */
       q += GS_NUM[SEL];
       k++;
     }
