@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--posting-store", action="store_true",
+                    help="time the §7.5 posting store (docIDs + TFs): the fused decode against "
+                         "two separate decodes")
     ap.add_argument("--spawn-check", action="store_true",
                     help="(tests) start --gpus ranks, all-reduce their ranks, print one line")
     ap.add_argument("--random-access", action="store_true",
@@ -710,6 +713,93 @@ def run_random_access(args, dev):
     print(json.dumps(line), flush=True)
 
 
+def run_posting_store(args, dev):
+    """--posting-store: §7.5's store (lists shorter than 64: Variable Byte) of the
+    headline config's lists with a term frequency per posting (seeded Geometric(0.4) draws,
+    a stand-in: the corpora are absent), every Group-Scheme variant in turn (config 2) or the
+    config's codecs: gc_decode_posting_store -- the long group's docIDs and TFs in ONE fused
+    k_decode pass -- against the same store decoded by separate calls (gc_decode_dgaps of
+    the docIDs, gc_decode of the TFs, and the Variable Byte groups), both with their index
+    stages; the outputs are compared."""
+    import torch
+    from paper_1502_01916_b200 import gc
+    zeta = tuple(int(x) for x in args.pfd_zeta.split("/"))
+    w, _, _ = make_workload(args, 0, 1)
+    rng = np.random.default_rng(2024)
+    tfs = (rng.geometric(0.4, w.n_ints) % 65536).astype(np.uint32)
+    stream = torch.cuda.current_stream(dev)
+    per, tot_f, tot_s, n_tot = {}, 0.0, 0.0, 0
+    for c, v, f, z in config_codecs(args.config, zeta):
+        if c == gc.VARBYTE:
+            continue
+        lab = gc.codec_label(c, v, f)
+        st = gc.encode_posting_store(w.values, w.list_n, c, v, delta=w.delta, tfs=tfs,
+                                     frame_quads=f, zeta=z)
+        parts = [gc.to_device(b, dev) for b in (st.long, st.tf_long, st.short, st.tf_short)]
+        out_d = torch.empty(max(st.total, 4), dtype=torch.int32, device=dev)
+        out_t = torch.empty_like(out_d)
+        wss = [gc.alloc_workspace(p, dev) for p in parts]
+
+        def separate():
+            gc.decode_dgaps(parts[0], out=out_d, ws=wss[0])
+            gc.decode(parts[1], out=out_t, ws=wss[1])
+            if st.short.total_out:
+                gc.decode_dgaps(parts[2], out=out_d[st.short_base:], ws=wss[2])
+                gc.decode(parts[3], out=out_t[st.short_base:], ws=wss[3])
+
+        def fused():
+            return gc.decode_posting_store(st, dgaps=True, device=dev)
+        d_f, t_f, fw = fused()
+        separate()
+        torch.cuda.synchronize(dev)
+        ok = bool(torch.equal(d_f, out_d[:st.total])) and bool(torch.equal(t_f, out_t[:st.total]))
+        ok = ok and all(gc.read_device_status(x) == 0 for x in fw)
+        # time the decode calls only (the device batches of the fused path are uploaded once)
+        from paper_1502_01916_b200.gc import CPostingStore, _lib, _stream_ptr
+        import ctypes as C
+        cs = [p.cstruct() for p in parts]
+        cst = CPostingStore(cs[0], cs[2], C.pointer(cs[1]), C.pointer(cs[3]), st.short_base)
+        need = C.c_uint64()
+        _lib().gc_posting_store_ws_size(C.byref(cst), C.byref(need))
+        fws = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
+
+        def fused_call():
+            r = _lib().gc_decode_posting_store(C.byref(cst), out_d.data_ptr(), out_t.data_ptr(), 1,
+                                               fws.data_ptr(), fws.numel(), _stream_ptr(None))
+            assert r == 0
+        times = {}
+        for name, fn in (("fused", fused_call), ("separate", separate)):
+            for _ in range(args.warmup):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            times[name] = e0.elapsed_time(e1) / args.steps
+        n = 2 * (st.long.total_out + st.short.total_out)
+        per[lab] = {"fused_ms": round(times["fused"], 5), "separate_ms": round(times["separate"], 5),
+                    "speedup": round(times["separate"] / times["fused"], 3),
+                    "fused_ints_per_s": n / (times["fused"] / 1e3), "verified": ok,
+                    "short_lists": int(st.short.n_lists), "long_lists": int(st.long.n_lists)}
+        tot_f += times["fused"]
+        tot_s += times["separate"]
+        n_tot += n
+        del parts, out_d, out_t, wss, fws, d_f, t_f, fw
+        torch.cuda.empty_cache()
+    line = {"metric": "decoded uint32 ints/sec of a posting store (docIDs + TFs, §7.5)",
+            "value": n_tot / (tot_f / 1e3), "unit": "ints/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_f, "higher_is_better": True, "dtype": "u32",
+            "data": "synthetic (TFs: seeded Geometric(0.4) per posting)",
+            "config": {"workload": w.name, "codecs": list(per), "threshold": 64,
+                       "path": "gc_decode_posting_store (index stages + fused docID/TF k_decode + "
+                               "Variable Byte) vs separate gc_decode_dgaps / gc_decode calls"},
+            "fused_vs_separate": {"fused_ms": tot_f, "separate_ms": tot_s, "speedup": tot_s / tot_f},
+            "per_codec": per}
+    print(json.dumps(line), flush=True)
+
+
 def spawn_check(rank, world):
     """--spawn-check: the rank plumbing alone (gloo on CPU, NCCL on GPUs): every rank
     all-reduces its rank id; rank 0 prints {"world", "rank_sum"}."""
@@ -742,13 +832,14 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.encode or args.random_access:
+    if args.encode or args.random_access or args.posting_store:
         import torch
         from paper_1502_01916_b200 import build
         build.build()
         torch.cuda.set_device(local_rank)
         if rank == 0:
-            (run_encode if args.encode else run_random_access)(args, torch.device("cuda", local_rank))
+            fn = run_encode if args.encode else (run_random_access if args.random_access else run_posting_store)
+            fn(args, torch.device("cuda", local_rank))
         return
     import torch
     from paper_1502_01916_b200 import build

@@ -154,7 +154,10 @@ gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t w
  *   GC_STAGE_INDEX  the control-stream scan kernel (subsystem (a)),
  *   GC_STAGE_DECODE the fused unpack / patch / d-gap-scan / store kernel.
  * stage_mask is any OR of the three; stages run in that order.  Calling the three
- * stages one after another on one stream is exactly gc_decode / gc_decode_dgaps. */
+ * stages one after another on one stream is exactly gc_decode / gc_decode_dgaps.
+ * The decode stage is one cooperative launch of min(tiles, SMs x resident CTAs) CTAs, each
+ * taking every grid-th 8192-int tile; the environment variable GC_DECODE_MAX_GRID, if set,
+ * caps that grid (a test knob: many tiles per CTA at small sizes; same results). */
 enum { GC_STAGE_RESET = 1, GC_STAGE_INDEX = 2, GC_STAGE_DECODE = 4, GC_STAGE_ALL = 7 };
 gc_status gc_decode_stage(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_bytes,
                           void* stream, int dgaps, int stage_mask);
@@ -205,6 +208,50 @@ gc_status gc_build_skip(const gc_batch* b, const uint32_t* docids, uint64_t* ski
 gc_status gc_decode_range(const gc_batch* b, const uint64_t* skip_off,
                           const gc_skip_entry* entries, uint32_t* out, uint64_t first,
                           uint64_t count, int dgaps, void* ws, uint64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Posting store (§7.5: "we use VByte to compress posting lists with less than 64
+ * postings"; §7.4: query processing decodes d-gaps and TFs).  A store keeps the
+ * long lists (>= threshold ints) in a Group-codec batch and the short ones in a Variable
+ * Byte batch, and optionally each list's term frequencies beside its docIDs, split and
+ * encoded the same way with no d-gap.  Decoded, the long group's ints come first and the
+ * short group's from short_base (a multiple of 4); list_out_off[l] locates list l.
+ *
+ * gc_posting_split (host, no launch): for list_n[n_lists] and the threshold, the lists of
+ * each group in order (long_ids[*n_long], short_ids[*n_short]; caller arrays of n_lists),
+ * list_out_off[n_lists] and *short_base.
+ * gc_posting_gather (host, no launch): the values of lists ids[n_ids], concatenated in
+ * that order into out (and their lengths into out_list_n), for the encoder.
+ * ------------------------------------------------------------------------- */
+gc_status gc_posting_split(const uint32_t* list_n, uint64_t n_lists, uint32_t threshold,
+                           uint64_t* long_ids, uint64_t* n_long, uint64_t* short_ids,
+                           uint64_t* n_short, uint64_t* list_out_off, uint64_t* short_base);
+gc_status gc_posting_gather(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists,
+                            const uint64_t* ids, uint64_t n_ids, uint32_t* out,
+                            uint32_t* out_list_n);
+
+/* A store on the device: the two groups of docIDs, and (or NULL) of TFs.  long_tfs must
+ * have the long docIDs' codec, variant and total_out (the same lists). */
+typedef struct {
+  gc_batch long_docs, short_docs;
+  const gc_batch* long_tfs;
+  const gc_batch* short_tfs;
+  uint64_t short_base;
+} gc_posting_store;
+
+/* Workspace bytes for gc_decode_posting_store (host only). */
+gc_status gc_posting_store_ws_size(const gc_posting_store* s, uint64_t* bytes);
+
+/* Decode a whole store: docs[short_base + total of the short group] receives the docIDs
+ * (dgaps != 0) or gaps, tfs (if the store has TFs) the raw TFs, both in the store's output
+ * layout.  The long group's docIDs and TFs are decoded in ONE fused k_decode pass over
+ * both batches (their tiles interleaved: the TF tiles' unpack fills the docID tiles'
+ * look-back latency); the short groups by the Variable Byte kernels.  Sticky device status
+ * bits: gc_posting_store_status.  Asynchronous on `stream`. */
+gc_status gc_decode_posting_store(const gc_posting_store* s, uint32_t* docs, uint32_t* tfs,
+                                  int dgaps, void* ws, uint64_t ws_bytes, void* stream);
+gc_status gc_posting_store_status(const gc_posting_store* s, const void* ws, uint32_t* host_bits,
+                                  void* stream);
 
 /* Copy the sticky GC_DEV_* bits of a workspace to *host_bits.  Synchronises
  * `stream`.  0 means the last decode on this workspace saw a well-formed batch. */

@@ -102,8 +102,19 @@ struct UnitsPerThread<C, std::void_t<decltype(C::kUnitsPerThread)>> {
 #ifndef GC_DECODE_MINB
 #define GC_DECODE_MINB 3
 #endif
-template <class C, bool DGAPS>
-__global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t* __restrict__ out) {
+// PAIR: one pass over two batches of one codec that share the output tiling -- a posting
+// store's docIDs (batch 0, d-gap scan) and term frequencies (batch 1, raw) -- their tiles
+// interleaved (virtual tile 2t = docIDs tile t, 2t+1 = TFs tile t): one launch, the same
+// CTAs, the TF tiles' unpack filling the docID tiles' look-back latency.
+template <class C, bool DGAPS, bool PAIR = false>
+__global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t* __restrict__ out0,
+                                                                Dev D1, uint32_t* __restrict__ out1) {
+  const Dev& D = D0;       // (the docIDs batch: the look-back and the deferred carry stores)
+  uint32_t* out = out0;
+  // virtual tile vt -> its batch and its tile index in that batch
+  auto bat = [&](uint32_t vt) -> const Dev& { return (PAIR && (vt & 1u)) ? D1 : D0; };
+  auto tix = [&](uint32_t vt) { return PAIR ? vt >> 1 : vt; };
+  const uint32_t nvt = PAIR ? 2 * D0.n_tiles_b : D0.n_tiles_b;
   extern __shared__ __align__(128) uint8_t sm[];
   uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS<C>::kOut);
   uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS<C>::kOut);
@@ -129,34 +140,38 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t kU = UnitsPerThread<C>::v;  // parse units per thread per parse chunk
-  const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
-  const uint64_t dend = D.data_off[D.n_lists];
-  const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
   uint32_t phase = 0, err = 0;
 
-  // Entries of `tile` -> s_e (one warp)
-  auto load_entries = [&](uint32_t tile) {
-    if (tile < D.n_tiles_b) {
+  // Entries of virtual tile vt -> s_e (one warp)
+  auto load_entries = [&](uint32_t vt) {
+    const Dev& B = bat(vt);
+    const uint32_t tile = tix(vt);
+    if (vt < nvt) {
       if (lane < 16) {
         reinterpret_cast<uint32_t*>(s_e)[lane] =
-            reinterpret_cast<const uint32_t*>(D.entries + tile)[lane];
-      } else if (tile + 1 < D.n_tiles_b) {
+            reinterpret_cast<const uint32_t*>(B.entries + tile)[lane];
+      } else if (tile + 1 < B.n_tiles_b) {
         reinterpret_cast<uint32_t*>(s_e)[lane] =
-            reinterpret_cast<const uint32_t*>(D.entries + tile + 1)[lane - 16];
+            reinterpret_cast<const uint32_t*>(B.entries + tile + 1)[lane - 16];
       }
     }
   };
   // One thread: the tile's stream ranges from s_e -> s_g[buf], and the bulk async copies
   // of its control / exception bytes (barrier 0) and data (barrier 1).  A tile past the
   // end or with bad entries arms both barriers with 0 bytes.
-  auto setup = [&](uint32_t tile, uint32_t buf) {
+  auto setup = [&](uint32_t vt, uint32_t buf) {
+    const Dev& D = bat(vt);
+    const uint32_t tile = tix(vt);
+    const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
+    const uint64_t dend = D.data_off[D.n_lists];
+    const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
     Geo& g = s_g[buf];
     const Entry& E0 = s_e[0];
     const Entry& E1 = s_e[1];
     const bool last = tile + 1 == D.n_tiles_b;
     g.ok = 0;
     uint32_t cbytes = 0, xbytes = 0, dbytes = 0;
-    if (tile < D.n_tiles_b) {
+    if (vt < nvt) {
       const uint64_t wa = E0.w, wb = last ? cend - 1 : E1.w;
       g.ok = (E0.valid && (last || E1.valid) && wb >= wa && wb < D.n_ctrl_words &&
               E0.l < D.n_lists && (last || (E1.l >= E0.l && E1.l < D.n_lists))) ? 1u : 0u;
@@ -281,10 +296,14 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
 
   uint32_t buf = 0;
   long long t_last = clock64();
-  for (uint32_t tile = first_tile; tile < D.n_tiles_b; tile += gridDim.x, buf ^= 1u) {
+  for (uint32_t vt = first_tile; vt < nvt; vt += gridDim.x, buf ^= 1u) {
     GC_T(0);
+    const Dev& D = bat(vt);                             // this tile's batch
+    uint32_t* const out = (PAIR && (vt & 1u)) ? out1 : out0;
+    const uint32_t tile = tix(vt);
+    const bool dg = DGAPS && !(PAIR && (vt & 1u));    // (TFs: no d-gap)
     // warp 1 prefetches the next tile's entries (read after this tile's unpack)
-    if (warp == 1) load_entries(tile + gridDim.x);
+    if (warp == 1) load_entries(vt + gridDim.x);
     if (tid == 0) s_reset0[buf ^ 1u] = kT;  // the next tile's
     const Geo& G = s_g[buf];
     const bool ok = G.ok;
@@ -376,7 +395,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
         lt_db[tid] = (uint32_t)(D.data_off[l] * 32ull - va * 32ull);
         lt_eb[tid] = C::kExc ? (uint32_t)(D.exc_off[l] - ea) : 0u;
         // a list that starts inside the tile resets the d-gap scan
-        if (DGAPS && n > 0 && klo == 0 && oref >= kHalo && oref < kHalo + kT) {
+        if (dg && n > 0 && klo == 0 && oref >= kHalo && oref < kHalo + kT) {
           atomicOr(&s_rst[(oref - kHalo) >> 5], 1u << ((oref - kHalo) & 31u));
           atomicMin(&s_reset0[buf], oref - kHalo);
         }
@@ -524,14 +543,14 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
     if (DGAPS && s_pend.on) flush_pending();  // (a tile that staged nothing)
     __syncthreads();  // the tile is staged; the staging buffers and the next entries are free
     // the next tile's copies overlap this tile's scan, look-back and stores
-    if (tid == 0) setup(tile + gridDim.x, buf ^ 1u);
+    if (tid == 0) setup(vt + gridDim.x, buf ^ 1u);
     GC_T(4);
 
     // ------------------------------------------------------------------ d-gap scan
     const uint32_t nvalid = ok ? (last ? (uint32_t)(D.total_out - tT) : kT) : 0u;
     const uint32_t nch = (nvalid + 3) / 4;
     Seg1 rcarry{0u, 0u};
-    if (DGAPS && ok) {
+    if (dg && ok) {
       // thread t scans tile positions [32t, 32t+32) (staging chunks kHalo/4 + 8t ..)
       uint32_t v[32];
       const uint32_t cb = kHalo / 4 + 8 * tid;
@@ -572,7 +591,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
       if (tid == 0)
         st_relaxed_u64(D.tiles_b + tile, ((uint64_t)(rcarry.f ? kFlagIncl : kFlagAgg) << 32) | rcarry.v);
       __syncthreads();
-    } else if (DGAPS && tid == 0) {
+    } else if (dg && tid == 0) {
       st_relaxed_u64(D.tiles_b + tile, ((uint64_t)kFlagIncl << 32));
     }
 
@@ -605,7 +624,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D, uint32_t*
         __stcs(o4 + c, s_out4[sw_chunk(kHalo / 4 + c)]);
       }
     };
-    if (DGAPS) {
+    if (dg) {
       const uint32_t reset0 = s_reset0[buf];
 #ifdef GC_ABL_NOFLUSH
       const bool need_carry = false;

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -724,6 +725,7 @@ gc_status check_batch(const gc_batch* b, bool device_ptrs) {
 // per-device property of a kernel) is set on every launch -- both cost microseconds.
 struct DevInfo {
   int dev, n_sm;
+  uint64_t max_grid;  // GC_DECODE_MAX_GRID (tests: several tiles per CTA at small sizes), 0 = none
 };
 gc_status device_info(DevInfo* di) {
   int dev = 0, major = 0;
@@ -732,27 +734,32 @@ gc_status device_info(DevInfo* di) {
       cudaDeviceGetAttribute(&di->n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return GC_ERR_CUDA;
   di->dev = dev;
+  const char* mg = getenv("GC_DECODE_MAX_GRID");
+  di->max_grid = mg ? strtoull(mg, nullptr, 10) : 0;
   if (major != 10) return GC_ERR_UNSUPPORTED_DEVICE;
   return di->n_sm > 0 ? GC_OK : GC_ERR_CUDA;
 }
 
 template <class C>
-gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages,
-                       const DevInfo& di) {
-  if (stages & GC_STAGE_INDEX) {
-    const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
-    k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)di.n_sm * 8), kThreads, 0, st>>>(D);
-    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-    k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
-    if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-  }
-  if (D.n_tiles_b == 0 || !(stages & GC_STAGE_DECODE)) return GC_OK;
+gc_status launch_index(const Dev& D, cudaStream_t st, const DevInfo& di) {
+  const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
+  k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)di.n_sm * 8), kThreads, 0, st>>>(D);
+  if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
+  k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+  return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
+}
+
+// k_decode over one batch, or (pair) over a docIDs batch D and a TFs batch *D1 together
+template <class C>
+gc_status launch_decode(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, const DevInfo& di,
+                        const Dev* D1 = nullptr, uint32_t* out1 = nullptr) {
+  if (D.n_tiles_b == 0) return GC_OK;
   const uint32_t smem = DS<C>::bytes();
 #ifdef GC_ABL_NODGAP
-  auto kern = k_decode<C, false>;
-#else
-  auto kern = dgaps ? k_decode<C, true> : k_decode<C, false>;
+  dgaps = false;
 #endif
+  auto kern = D1 ? (dgaps ? k_decode<C, true, true> : k_decode<C, false, true>)
+                 : (dgaps ? k_decode<C, true, false> : k_decode<C, false, false>);
   int per_sm = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDT, smem) != cudaSuccess)
@@ -760,14 +767,66 @@ gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st,
   if (per_sm < 1) return GC_ERR_CUDA;  // (cannot happen on sm_100: the kernel fits one SM)
   // tiles are assigned round-robin to a co-resident grid (the decoupled look-back waits on
   // earlier tiles, which must all be running): a cooperative launch guarantees residency
-  const unsigned grid = (unsigned)mn64(D.n_tiles_b, (uint64_t)di.n_sm * per_sm);
-  if (grid == 0) return GC_OK;
-  Dev Dv = D;
-  void* args[] = {&Dv, &out};
+  const uint64_t nvt = D1 ? 2ull * D.n_tiles_b : D.n_tiles_b;
+  uint64_t cap = (uint64_t)di.n_sm * per_sm;
+  if (di.max_grid) cap = mn64(cap, di.max_grid);
+  // a pair's CTAs take every grid-th virtual tile: an odd stride alternates each CTA between
+  // docID tiles (d-gap scan, look-back) and TF tiles, where an even one would leave half the
+  // grid on the cheaper TF tiles and the docIDs on the other half
+  if (D1 && cap < nvt && (cap & 1) == 0 && cap > 1) cap--;
+  const unsigned grid = (unsigned)mn64(nvt, cap);
+  Dev Dv = D, Dv1 = D1 ? *D1 : D;
+  uint32_t* o1 = D1 ? out1 : out;
+  void* args[] = {&Dv, &out, &Dv1, &o1};
   if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kDT), args, smem, st) !=
       cudaSuccess)
     return GC_ERR_CUDA;
   return GC_OK;
+}
+
+template <class C>
+gc_status launch_codec(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages,
+                       const DevInfo& di) {
+  if (stages & GC_STAGE_INDEX) {
+    const gc_status s = launch_index<C>(D, st, di);
+    if (s != GC_OK) return s;
+  }
+  if (!(stages & GC_STAGE_DECODE)) return GC_OK;
+  return launch_decode<C>(D, out, dgaps, st, di);
+}
+
+template <class T>
+struct Tag {  // (a codec type as a value, for generic lambdas)
+  using type = T;
+};
+
+// The kernels' view of a batch and its workspace.
+Dev make_dev(const gc_batch* b, uint8_t* w, const WsLayout& L) {
+  Dev D;
+  D.n_lists = b->n_lists;
+  D.list_n = b->list_n;
+  D.ctrl_off = b->ctrl_off;
+  D.data_off = b->data_off;
+  D.exc_off = b->codec == GC_GROUP_PFD ? b->exc_off : nullptr;
+  D.out_off = b->out_off;
+  D.ctrl_words = (const uint32_t*)b->ctrl;
+  D.n_ctrl_words = b->ctrl_bytes / 4;
+  D.data = (const uint4*)b->data;
+  D.data_vectors = b->data_vectors;
+  D.exc = b->exc;
+  D.exc_bytes = b->exc_bytes;
+  D.total_out = b->total_out;
+  D.n_tiles_a = (uint32_t)L.n_tiles_a;
+  D.n_tiles_b = (uint32_t)L.n_tiles_b;
+  D.hdr = (WsHeader*)w;
+  D.tiles_a = (TileA*)(w + L.off_tiles_a);
+  D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
+  D.entries = (Entry*)(w + L.off_entries);
+  D.first_list = (uint32_t*)(w + L.off_first);
+  D.docids = nullptr;
+  D.skip_off = nullptr;
+  D.skip = nullptr;
+  return D;
 }
 
 // What one call does: a decode (its stages), the skip-table build, or a range decode.
@@ -825,27 +884,7 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   if (J.kind == JOB_SKIP && b->n_lists == 0)
     return cudaMemsetAsync(skip_off_out, 0, 8, st) == cudaSuccess ? GC_OK : GC_ERR_CUDA;
   if (b->n_lists == 0 || b->total_out == 0 || (J.kind == JOB_RANGE && J.last <= J.first)) return GC_OK;
-  Dev D;
-  D.n_lists = b->n_lists;
-  D.list_n = b->list_n;
-  D.ctrl_off = b->ctrl_off;
-  D.data_off = b->data_off;
-  D.exc_off = b->codec == GC_GROUP_PFD ? b->exc_off : nullptr;
-  D.out_off = b->out_off;
-  D.ctrl_words = (const uint32_t*)b->ctrl;
-  D.n_ctrl_words = b->ctrl_bytes / 4;
-  D.data = (const uint4*)b->data;
-  D.data_vectors = b->data_vectors;
-  D.exc = b->exc;
-  D.exc_bytes = b->exc_bytes;
-  D.total_out = b->total_out;
-  D.n_tiles_a = (uint32_t)L.n_tiles_a;
-  D.n_tiles_b = (uint32_t)L.n_tiles_b;
-  D.hdr = (WsHeader*)w;
-  D.tiles_a = (TileA*)(w + L.off_tiles_a);
-  D.tiles_b = (uint64_t*)(w + L.off_tiles_b);
-  D.entries = (Entry*)(w + L.off_entries);
-  D.first_list = (uint32_t*)(w + L.off_first);
+  Dev D = make_dev(b, w, L);
   D.docids = docids;
   D.skip_off = J.kind == JOB_SKIP ? skip_off_out : const_cast<uint64_t*>(skip_off_in);
   D.skip = skip;
@@ -953,6 +992,171 @@ gc_status gc_decode_range(const gc_batch* b, const uint64_t* skip_off,
   return decode_impl(b, out, ws, ws_bytes, stream,
                      Job{JOB_RANGE, dgaps != 0, GC_STAGE_DECODE, first, first + count}, nullptr,
                      skip_off, nullptr, const_cast<gc_skip_entry*>(entries));
+}
+
+// ------------------------------------------------------------------ posting store
+gc_status gc_posting_split(const uint32_t* list_n, uint64_t n_lists, uint32_t threshold,
+                           uint64_t* long_ids, uint64_t* n_long, uint64_t* short_ids,
+                           uint64_t* n_short, uint64_t* list_out_off, uint64_t* short_base) {
+  if ((n_lists && (!list_n || !long_ids || !short_ids || !list_out_off)) || !n_long || !n_short ||
+      !short_base)
+    return GC_ERR_INVALID_ARGUMENT;
+  uint64_t nl = 0, ns = 0, long_total = 0;
+  for (uint64_t l = 0; l < n_lists; l++) {
+    if (list_n[l] >= threshold) {
+      long_ids[nl++] = l;
+      list_out_off[l] = long_total;
+      long_total += list_n[l];
+    } else {
+      short_ids[ns++] = l;
+    }
+  }
+  const uint64_t base = (long_total + 3) & ~3ull;  // the short group starts 16-B aligned
+  uint64_t off = base;
+  for (uint64_t i = 0; i < ns; i++) {
+    list_out_off[short_ids[i]] = off;
+    off += list_n[short_ids[i]];
+  }
+  *n_long = nl;
+  *n_short = ns;
+  *short_base = base;
+  return GC_OK;
+}
+
+gc_status gc_posting_gather(const uint32_t* values, const uint32_t* list_n, uint64_t n_lists,
+                            const uint64_t* ids, uint64_t n_ids, uint32_t* out,
+                            uint32_t* out_list_n) {
+  if ((n_ids && (!ids || !out_list_n)) || (n_lists && !list_n)) return GC_ERR_INVALID_ARGUMENT;
+  // list starts, then each requested list copied in turn
+  uint64_t* start = (uint64_t*)malloc((size_t)(n_lists + 1) * 8);
+  if (!start) return GC_ERR_NOMEM;
+  start[0] = 0;
+  for (uint64_t l = 0; l < n_lists; l++) start[l + 1] = start[l] + list_n[l];
+  uint64_t o = 0;
+  gc_status st = GC_OK;
+  for (uint64_t i = 0; i < n_ids; i++) {
+    if (ids[i] >= n_lists) {
+      st = GC_ERR_INVALID_ARGUMENT;
+      break;
+    }
+    const uint32_t n = list_n[ids[i]];
+    if (n && (!values || !out)) {
+      st = GC_ERR_INVALID_ARGUMENT;
+      break;
+    }
+    if (n) memcpy(out + o, values + start[ids[i]], (size_t)n * 4);
+    out_list_n[i] = n;
+    o += n;
+  }
+  free(start);
+  return st;
+}
+
+static uint64_t store_tf_ws_off(const gc_posting_store* s) {
+  return (ws_layout(&s->long_docs).bytes + 255) & ~255ull;
+}
+
+gc_status gc_posting_store_ws_size(const gc_posting_store* s, uint64_t* bytes) {
+  if (!s || !bytes) return GC_ERR_INVALID_ARGUMENT;
+  *bytes = store_tf_ws_off(s) + (s->long_tfs ? ws_layout(s->long_tfs).bytes : sizeof(WsHeader));
+  return GC_OK;
+}
+
+gc_status gc_decode_posting_store(const gc_posting_store* s, uint32_t* docs, uint32_t* tfs,
+                                  int dgaps, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!s || !ws || !aligned16(ws)) return GC_ERR_INVALID_ARGUMENT;
+  uint64_t need = 0;
+  gc_posting_store_ws_size(s, &need);
+  if (ws_bytes < need) return GC_ERR_WORKSPACE_TOO_SMALL;
+  const gc_batch* LD = &s->long_docs;
+  const gc_batch* SD = &s->short_docs;
+  const bool has_tf = s->long_tfs != nullptr;
+  if (has_tf && (!tfs || !s->short_tfs)) return GC_ERR_INVALID_ARGUMENT;
+  if (SD->codec != GC_VARBYTE || (has_tf && s->short_tfs->codec != GC_VARBYTE)) return GC_ERR_BAD_VARIANT;
+  if ((s->short_base & 3) || s->short_base < LD->total_out) return GC_ERR_INVALID_ARGUMENT;
+  if (has_tf && (s->long_tfs->codec != LD->codec || s->long_tfs->variant != LD->variant ||
+                 s->long_tfs->pfd_frame_quads != LD->pfd_frame_quads ||
+                 s->long_tfs->total_out != LD->total_out || s->long_tfs->n_lists != LD->n_lists))
+    return GC_ERR_INVALID_ARGUMENT;
+  for (const gc_batch* b : {LD, SD, s->long_tfs, s->short_tfs}) {
+    if (!b) continue;
+    gc_status st = check_batch(b, true);
+    if (st != GC_OK) return st;
+  }
+  if (!docs || !aligned16(docs) || (has_tf && !aligned16(tfs))) return GC_ERR_INVALID_ARGUMENT;
+  DevInfo di;
+  gc_status st = device_info(&di);
+  if (st != GC_OK) return st;
+  cudaStream_t cs = (cudaStream_t)stream;
+  uint8_t* w0 = (uint8_t*)ws;
+  uint8_t* w1 = w0 + store_tf_ws_off(s);
+  const WsLayout L0 = ws_layout(LD);
+  const WsLayout L1 = has_tf ? ws_layout(s->long_tfs) : WsLayout{};
+  if (cudaMemsetAsync(w0, 0, L0.bytes, cs) != cudaSuccess ||
+      cudaMemsetAsync(w1, 0, has_tf ? L1.bytes : sizeof(WsHeader), cs) != cudaSuccess)
+    return GC_ERR_CUDA;
+  Dev D0 = make_dev(LD, w0, L0);
+  Dev D1 = has_tf ? make_dev(s->long_tfs, w1, L1) : D0;
+  // the long group: both index stages, then one fused decode of docIDs (+ TFs)
+  auto run_long = [&](auto codec_tag) -> gc_status {
+    using C = typename decltype(codec_tag)::type;
+    gc_status r = launch_index<C>(D0, cs, di);
+    if (r == GC_OK && has_tf) r = launch_index<C>(D1, cs, di);
+    if (r != GC_OK) return r;
+    return launch_decode<C>(D0, docs, dgaps != 0, cs, di, has_tf ? &D1 : nullptr, tfs);
+  };
+  if (LD->n_lists && LD->total_out) {
+    if (LD->codec == GC_VARBYTE) return GC_ERR_BAD_VARIANT;
+    switch (LD->codec) {
+      case GC_GROUP_SIMPLE: st = run_long(Tag<CodecGS>{}); break;
+      case GC_GROUP_AFOR: st = run_long(Tag<CodecAFOR>{}); break;
+      case GC_GROUP_PFD:
+        if (LD->variant == 1)
+          st = LD->pfd_frame_quads == 32 ? run_long(Tag<CodecPFD<32, false>>{})
+                                         : run_long(Tag<CodecPFD<128, false>>{});
+        else
+          st = LD->pfd_frame_quads == 32 ? run_long(Tag<CodecPFD<32>>{})
+                                         : run_long(Tag<CodecPFD<128>>{});
+        break;
+      default:
+        switch (LD->variant) {
+          case 0: st = run_long(Tag<CodecGscB<1>>{}); break;
+          case 1: st = run_long(Tag<CodecGscB<2>>{}); break;
+          case 2: st = run_long(Tag<CodecGscB<4>>{}); break;
+          case 3: st = run_long(Tag<CodecGscB<8>>{}); break;
+          case 4: st = run_long(Tag<CodecGscCU<1>>{}); break;
+          case 5: st = run_long(Tag<CodecGscCU<2>>{}); break;
+          case 6: st = run_long(Tag<CodecGscCU<4>>{}); break;
+          case 7: st = run_long(Tag<CodecGscCU<8>>{}); break;
+          case 10: st = run_long(Tag<CodecGscIU<4>>{}); break;
+          case 11: st = run_long(Tag<CodecGscIU<8>>{}); break;
+          default: st = GC_ERR_BAD_VARIANT;
+        }
+    }
+    if (st != GC_OK) return st;
+  }
+  // the short group: Variable Byte, docIDs and TFs, from short_base (status: same headers)
+  if (SD->n_lists && SD->total_out) {
+    const WsLayout LS = ws_layout(SD);
+    Dev DS = make_dev(SD, w0, LS);
+    st = launch_varbyte(DS, docs + s->short_base, dgaps != 0, cs, GC_STAGE_DECODE, di.n_sm);
+    if (st != GC_OK) return st;
+    if (has_tf) {
+      Dev DT = make_dev(s->short_tfs, w1, ws_layout(s->short_tfs));
+      st = launch_varbyte(DT, tfs + s->short_base, false, cs, GC_STAGE_DECODE, di.n_sm);
+    }
+  }
+  return st;
+}
+
+gc_status gc_posting_store_status(const gc_posting_store* s, const void* ws, uint32_t* host_bits,
+                                  void* stream) {
+  if (!s || !ws || !host_bits) return GC_ERR_INVALID_ARGUMENT;
+  uint32_t a = 0, b = 0;
+  gc_status st = gc_read_device_status(ws, &a, stream);
+  if (st == GC_OK) st = gc_read_device_status((const uint8_t*)ws + store_tf_ws_off(s), &b, stream);
+  *host_bits = a | b;
+  return st;
 }
 
 gc_status gc_read_device_status(const void* ws, uint32_t* host_bits, void* stream) {

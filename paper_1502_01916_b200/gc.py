@@ -62,6 +62,11 @@ def _lib():
             "gc_decode_stage": (i32, [P(CBatch), vp, vp, u64, vp, i32, i32]),
             "gc_decode_range": (i32, [P(CBatch), vp, vp, vp, u64, u64, i32, vp, u64, vp]),
             "gc_skip_capacity": (i32, [P(CBatch), P(u64)]),
+            "gc_posting_split": (i32, [vp, u64, C.c_uint32, vp, P(u64), vp, P(u64), vp, P(u64)]),
+            "gc_posting_gather": (i32, [vp, vp, u64, vp, u64, vp, vp]),
+            "gc_posting_store_ws_size": (i32, [P(CPostingStore), P(u64)]),
+            "gc_decode_posting_store": (i32, [P(CPostingStore), vp, vp, i32, vp, u64, vp]),
+            "gc_posting_store_status": (i32, [P(CPostingStore), vp, P(C.c_uint32), vp]),
             "gc_build_skip": (i32, [P(CBatch), vp, vp, vp, vp, u64, vp]),
             "gc_read_device_status": (i32, [vp, P(C.c_uint32), vp]),
             "gc_checksum": (i32, [P(CBatch), vp, u64, vp, vp]),
@@ -302,69 +307,87 @@ def encode_posting_store(values: np.ndarray, list_n: np.ndarray, codec: int, var
                          delta: bool = False, threshold: int = 64, tfs: "np.ndarray | None" = None,
                          **kw) -> PostingStore:
     """`tfs` (optional, one per posting): the lists' term frequencies, stored beside the
-    docIDs with the same split and codecs but no d-gap (TFs are not sorted)."""
+    docIDs with the same split and codecs but no d-gap (TFs are not sorted).  The
+    split and gather are gc_posting_split / gc_posting_gather; each group is encoded by the
+    host encoder."""
     v = np.ascontiguousarray(values, np.uint32)
     ln = np.ascontiguousarray(list_n, np.uint32)
-    starts = np.concatenate([[0], np.cumsum(ln.astype(np.int64))[:-1]]) if len(ln) else np.zeros(0, np.int64)
-    is_short = ln < threshold
-    idx = {True: np.nonzero(is_short)[0], False: np.nonzero(~is_short)[0]}
+    L = len(ln)
+    ids = {True: np.zeros(max(L, 1), np.uint64), False: np.zeros(max(L, 1), np.uint64)}
+    n_long, n_short, base = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    off = np.zeros(max(L, 1), np.uint64)
+    st = _lib().gc_posting_split(ln.ctypes.data if L else None, L, threshold,
+                                 ids[False].ctypes.data, C.byref(n_long), ids[True].ctypes.data,
+                                 C.byref(n_short), off.ctypes.data, C.byref(base))
+    if st:
+        raise GcError(st, "gc_posting_split")
+    groups = {False: ids[False][:n_long.value], True: ids[True][:n_short.value]}
 
-    def gather(ids):
-        if len(ids) == 0:
-            return np.zeros(0, np.uint32)
-        return np.concatenate([v[starts[i]:starts[i] + ln[i]] for i in ids])
-    longb = encode_batch(gather(idx[False]), ln[idx[False]], codec, variant, delta=delta, **kw)
-    shortb = encode_batch(gather(idx[True]), ln[idx[True]], VARBYTE, 0, delta=delta)
-    short_base = (longb.total_out + 3) & ~3
-    off = np.zeros(len(ln), np.uint64)
-    off[idx[False]] = longb.out_off[:-1]
-    off[idx[True]] = short_base + shortb.out_off[:-1]
-    st = PostingStore(longb, shortb, off, short_base, short_base + shortb.total_out)
+    def gather(src, short):
+        g = groups[short]
+        n = int(ln[g.astype(np.int64)].sum()) if len(g) else 0
+        out = np.zeros(max(n, 1), np.uint32)
+        gl = np.zeros(max(len(g), 1), np.uint32)
+        r = _lib().gc_posting_gather(src.ctypes.data if src.size else None, ln.ctypes.data if L else None,
+                                     L, g.ctypes.data if len(g) else None, len(g), out.ctypes.data,
+                                     gl.ctypes.data)
+        if r:
+            raise GcError(r, "gc_posting_gather")
+        return out[:n], gl[:len(g)]
+    longb = encode_batch(*gather(v, False), codec, variant, delta=delta, **kw)
+    shortb = encode_batch(*gather(v, True), VARBYTE, 0, delta=delta)
+    short_base = int(base.value)
+    st_ = PostingStore(longb, shortb, off[:L], short_base, short_base + shortb.total_out)
     if tfs is not None:
         t = np.ascontiguousarray(tfs, np.uint32)
         assert t.size == v.size, "one TF per posting"
-
-        def gather_t(ids):
-            if len(ids) == 0:
-                return np.zeros(0, np.uint32)
-            return np.concatenate([t[starts[i]:starts[i] + ln[i]] for i in ids])
-        st.tf_long = encode_batch(gather_t(idx[False]), ln[idx[False]], codec, variant, **kw)
-        st.tf_short = encode_batch(gather_t(idx[True]), ln[idx[True]], VARBYTE, 0)
-    return st
+        st_.tf_long = encode_batch(*gather(t, False), codec, variant, **kw)
+        st_.tf_short = encode_batch(*gather(t, True), VARBYTE, 0)
+    return st_
 
 
-def _decode_groups(batches, total, short_base, dgaps, device, stream):
-    import torch
-    out = torch.empty(max(total, 4), dtype=torch.int32, device=device)
-    fn = decode_dgaps if dgaps else decode
-    wss = []
-    for hb, base in zip(batches, (0, short_base)):
-        db = to_device(hb, device)
-        ws = alloc_workspace(db, device)
-        fn(db, out=out[base:base + max(hb.total_out, 4)] if hb.total_out else out, ws=ws,
-           stream=stream)
-        wss.append(ws)
-    return out[:total], tuple(wss)
+class CPostingStore(C.Structure):
+    _fields_ = [("long_docs", CBatch), ("short_docs", CBatch), ("long_tfs", C.POINTER(CBatch)),
+                ("short_tfs", C.POINTER(CBatch)), ("short_base", C.c_uint64)]
+
+
+class StoreStatus(tuple):
+    """(ws of the docIDs, ws of the TFs) views of the one workspace; keeps the device
+    batches alive for as long as the caller holds it."""
 
 
 def decode_posting_store(store: PostingStore, dgaps: bool = True, device="cuda", stream=None):
-    """Both groups decoded into one output (int32 view of uint32): the long group with its
-    codec, the short group with Variable Byte.  Returns (out, (ws_long, ws_short)); with
-    TFs in the store, returns (docs, tfs, workspaces): the TFs (no d-gap) are decoded on a
-    second stream, concurrently with the docIDs (two decodes, not one fused kernel)."""
+    """gc_decode_posting_store: the long group's docIDs (and TFs: one fused k_decode pass
+    over both batches) and the short group's (Variable Byte) into one output (int32 view of
+    uint32).  Returns (docs, workspaces) or, with TFs in the store, (docs, tfs, workspaces);
+    gc.read_device_status(w) == 0 for both workspaces means a clean decode."""
+    import contextlib
     import torch
-    if store.tf_long is None:
-        return _decode_groups((store.long, store.short), store.total, store.short_base, dgaps,
-                              device, stream)
-    main = torch.cuda.current_stream(device) if stream is None else stream
-    tfs_stream = torch.cuda.Stream(device)
-    tfs_stream.wait_stream(main)
-    docs, w1 = _decode_groups((store.long, store.short), store.total, store.short_base, dgaps,
-                              device, main)
-    tfs, w2 = _decode_groups((store.tf_long, store.tf_short), store.total, store.short_base,
-                             False, device, tfs_stream)
-    main.wait_stream(tfs_stream)
-    return docs, tfs, w1 + w2
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:  # (everything allocated on the decoding stream: no early reuse of its memory)
+        has_tf = store.tf_long is not None
+        dbs = [to_device(b, device) for b in
+               ((store.long, store.short, store.tf_long, store.tf_short) if has_tf
+                else (store.long, store.short))]
+        cs = [d.cstruct() for d in dbs]
+        cst = CPostingStore(cs[0], cs[1], C.pointer(cs[2]) if has_tf else None,
+                            C.pointer(cs[3]) if has_tf else None, store.short_base)
+        need = C.c_uint64()
+        _lib().gc_posting_store_ws_size(C.byref(cst), C.byref(need))
+        ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=device)
+        docs = torch.empty(max(store.total, 4), dtype=torch.int32, device=device)
+        tfs = torch.empty(max(store.total, 4), dtype=torch.int32, device=device) if has_tf else None
+        st = _lib().gc_decode_posting_store(C.byref(cst), docs.data_ptr(),
+                                            tfs.data_ptr() if has_tf else None, int(dgaps),
+                                            ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        if st:
+            raise GcError(st, "gc_decode_posting_store")
+    off = (workspace_size(dbs[0]) + 255) & ~255
+    w = StoreStatus((ws[:off], ws[off:]))
+    w.batches = dbs
+    if has_tf:
+        return docs[:store.total], tfs[:store.total], w
+    return docs[:store.total], w
 
 
 def to_device(hb: HostBatch, device="cuda", pin: bool = False) -> DeviceBatch:

@@ -375,6 +375,76 @@ def test_decode_range_flags_a_bad_table():
     assert gc.read_device_status(ws) & 16
 
 
+@pytest.mark.parametrize("codec,variant", [(O.GROUP_SCHEME, O.gsc_variant(8, "IU")), (O.GROUP_PFD, 0),
+                                           (O.GROUP_AFOR, 0), (O.GROUP_SIMPLE, 0),
+                                           (O.GROUP_SCHEME, O.gsc_variant(1, "CU")), (O.GROUP_PFD, 1)])
+def test_fused_docid_tf_decode_equals_the_oracle(codec, variant):
+    """gc_decode_posting_store's fused pass (one k_decode over the docIDs batch and the TFs
+    batch, their tiles interleaved) against the oracle's decode of each batch: docIDs with
+    the d-gap scan, TFs raw; long lists spanning many tiles so both look-back and the
+    interleaving are exercised."""
+    rng = np.random.default_rng(40 + codec + 16 * variant)
+    w = gen.random_lists(rng, 40, 60000, 20, 0.01)
+    docs = np.zeros(w.n_ints, np.uint32)
+    starts = np.concatenate([[0], np.cumsum(w.list_n.astype(np.int64))])
+    for i in range(len(w.list_n)):  # strictly increasing docIDs per list
+        seg = w.values[starts[i]:starts[i + 1]].astype(np.uint64) % 1000 + 1
+        docs[starts[i]:starts[i + 1]] = (np.cumsum(seg) % (1 << 32)).astype(np.uint32)
+    tfs = (rng.geometric(0.3, w.n_ints) % 5000).astype(np.uint32)
+    st = gc.encode_posting_store(docs, w.list_n, codec, variant, delta=True, tfs=tfs)
+    d, t, wss = gc.decode_posting_store(st, dgaps=True)
+    torch.cuda.synchronize()
+    assert all(gc.read_device_status(x) == 0 for x in wss)
+    want_d = O.decode_batch(st.long.as_dict(), dgaps=True, threads=4)
+    want_t = O.decode_batch(st.tf_long.as_dict(), dgaps=False, threads=4)
+    n = st.long.total_out
+    assert np.array_equal(d[:n].cpu().numpy().view(np.uint32), want_d)
+    assert np.array_equal(t[:n].cpu().numpy().view(np.uint32), want_t)
+    if st.short.total_out:
+        sb = st.short_base
+        assert np.array_equal(d[sb:sb + st.short.total_out].cpu().numpy().view(np.uint32),
+                              O.decode_batch(st.short.as_dict(), dgaps=True, threads=4))
+        assert np.array_equal(t[sb:sb + st.short.total_out].cpu().numpy().view(np.uint32),
+                              O.decode_batch(st.tf_short.as_dict(), dgaps=False, threads=4))
+    for i in range(len(w.list_n)):
+        o, k = int(st.list_out_off[i]), int(w.list_n[i])
+        assert np.array_equal(t[o:o + k].cpu().numpy().view(np.uint32), tfs[starts[i]:starts[i] + k])
+
+
+@pytest.mark.parametrize("max_grid", ["7", "8", "1"])
+def test_fused_decode_with_many_tiles_per_cta(max_grid, monkeypatch):
+    """The fused pair with more tiles than CTAs (GC_DECODE_MAX_GRID caps the grid): an odd
+    grid alternates every CTA between docID and TF tiles (a docID tile's deferred carry
+    stores then run inside a TF tile), the library makes an even cap odd, and one CTA walks
+    all tiles in order; the plain decode under the same caps as well."""
+    monkeypatch.setenv("GC_DECODE_MAX_GRID", max_grid)
+    rng = np.random.default_rng(71)
+    w = gen.random_lists(rng, 30, 20000, 18, 0.02)
+    docs = np.zeros(w.n_ints, np.uint32)
+    starts = np.concatenate([[0], np.cumsum(w.list_n.astype(np.int64))])
+    for i in range(len(w.list_n)):
+        seg = w.values[starts[i]:starts[i + 1]].astype(np.uint64) % 3000 + 1
+        docs[starts[i]:starts[i + 1]] = (np.cumsum(seg) % (1 << 32)).astype(np.uint32)
+    tfs = (rng.geometric(0.3, w.n_ints) % 5000).astype(np.uint32)
+    for codec, variant in [(O.GROUP_SCHEME, O.gsc_variant(1, "CU")), (O.GROUP_PFD, 0), (O.GROUP_AFOR, 0)]:
+        st = gc.encode_posting_store(docs, w.list_n, codec, variant, delta=True, tfs=tfs)
+        d, t, wss = gc.decode_posting_store(st, dgaps=True)
+        torch.cuda.synchronize()
+        assert all(gc.read_device_status(x) == 0 for x in wss)
+        n = st.long.total_out
+        assert n > 20 * 8192
+        assert np.array_equal(d[:n].cpu().numpy().view(np.uint32),
+                              O.decode_batch(st.long.as_dict(), dgaps=True, threads=4))
+        assert np.array_equal(t[:n].cpu().numpy().view(np.uint32),
+                              O.decode_batch(st.tf_long.as_dict(), dgaps=False, threads=4))
+        db = gc.to_device(st.long)
+        out, ws = gc.decode_dgaps(db)
+        torch.cuda.synchronize()
+        assert gc.read_device_status(ws) == 0
+        assert np.array_equal(out[:n].cpu().numpy().view(np.uint32),
+                              O.decode_batch(st.long.as_dict(), dgaps=True, threads=4))
+
+
 def test_posting_store_with_term_frequencies():
     """The posting store with TF streams beside the docIDs (§8(f) rank 3): TFs (small, not
     sorted: Geometric(0.5)) decoded raw, concurrently with the d-gap docIDs."""
