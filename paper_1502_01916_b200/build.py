@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES_CU = ["gc_kernels.cu", "gc_encode_gpu.cu"]
 SOURCES_CPP = ["gc_encoder.cpp"]
-HEADERS = ["gc_codecs.cuh", "gc_device.cuh", "gc_decode.cuh"]
+HEADERS = ["gc_codecs.cuh", "gc_device.cuh", "gc_decode.cuh", "gc_skip.cuh"]
 
 
 def _stale() -> bool:

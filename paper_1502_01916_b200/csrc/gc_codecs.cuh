@@ -19,6 +19,9 @@
 
 #include "gc_device.cuh"
 
+#ifndef GC_AFOR_SUB
+#define GC_AFOR_SUB 1  // Group-AFOR parse units per frame header (4: 8-quad parts, measured 6% slower)
+#endif
 #ifndef GC_FRAME_UPT
 #define GC_FRAME_UPT 2  // parse units per thread per chunk for the frame codecs (AFOR, PFD)
 #endif
@@ -140,11 +143,30 @@ struct CodecGscB {
     if (CG == 4) return (w >> (8 * (k / 2) + 3 * (k % 2))) & 7u;
     return (w >> (2 * k)) & 3u;
   }
-  __device__ static WAgg agg(const WCtx& c) {
-    uint32_t d = 0;
+  // Eq. (2) summed over fields by bit planes: sum of the field values = sum over bits b of
+  // 2^b x popc(bit b of every field) (a handful of popcounts instead of a loop over fields)
+  static constexpr int kFW = CG == 1 ? 5 : (CG == 2 ? 4 : (CG == 4 ? 3 : 2));  // field bits
+  __host__ __device__ static constexpr uint32_t fpos(int k) {
+    return CG == 1 ? 16 * (k / 3) + 5 * (k % 3) : (CG == 2 ? 4 * k : (CG == 4 ? 8 * (k / 2) + 3 * (k % 2) : 2 * k));
+  }
+  __host__ __device__ static constexpr uint32_t plane(int b, int nf) {  // bit b of fields 0 .. nf-1
+    uint32_t m = 0;
+    for (int k = 0; k < nf; k++) m |= 1u << (fpos(k) + b);
+    return m;
+  }
+  __device__ static __forceinline__ uint32_t field_sum(uint32_t x, int nf) {
+    uint32_t t = 0;
 #pragma unroll
-    for (int k = 0; k < kPF; k++) d += CG * (field(c.w, c.part * kPF + k) + 1);  // Eq. (2)
-    return WAgg{(uint32_t)kPF, d, 0u};
+    for (int b = 0; b < kFW; b++) t += (uint32_t)__popc(x & plane(b, nf)) << b;
+    return t;
+  }
+  __device__ static WAgg agg(const WCtx& c) {
+    // part p's fields sit 32/kParts bits above part 0's (every CG)
+    const uint32_t x = c.w >> ((32 / kParts) * c.part);
+    return WAgg{(uint32_t)kPF, CG * (field_sum(x, kPF) + kPF), 0u};
+  }
+  __device__ static WAgg word_agg_fast(const WCtx& c) {
+    return WAgg{(uint32_t)kFields, CG * (field_sum(c.w, kFields) + kFields), 0u};
   }
   __device__ static bool suspect(const WCtx&) { return false; }  // every field value is valid
   // emit(j, pos, bw) for the quads j in [qa, qb) of this unit (q, d: the unit's prefix)
@@ -383,9 +405,13 @@ struct CodecGscIU {
 // Header byte (A22): bits 0-1 length code (8/16/32 quads), bits 2-6 bw-1, bit 7 = 0.
 // Each frame starts a fresh 128-bit vector: ceil(L*bw/32) vectors.
 struct CodecAFOR {
+  // a parse unit = one 8-quad part of a frame (frames hold 8, 16 or 32 quads): a
+  // header byte per frame, kSub parts per header (those past the frame's length are empty),
+  // so a tile of long frames still gives every thread work
+  static constexpr uint32_t kSub = GC_AFOR_SUB;
   static constexpr bool kExc = false;
   static constexpr uint64_t kBackBits = 0;
-  static constexpr int kParts = 4;           // a parse unit = one frame header byte
+  static constexpr int kParts = 4 * kSub;
   static constexpr uint32_t kUnitsPerThread = GC_FRAME_UPT;
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
@@ -394,22 +420,53 @@ struct CodecAFOR {
     L = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
     bw = ((h >> 2) & 31u) + 1u;
   }
+  // part p: header p / kSub, frame quads [8 s, 8 s + 8) with s = p % kSub (kSub = 1: the
+  // whole frame); the frame's padding to whole vectors goes to its last part
+  __device__ static __forceinline__ void part(const WCtx& c, uint32_t& h, uint32_t& nq, uint32_t& bw,
+                                              uint32_t& d) {
+    h = (c.w >> (8 * (c.part / kSub))) & 0xFFu;
+    uint32_t L;
+    frame(h, L, bw);
+    const uint32_t dlen = 32u * ((L * bw + 31u) / 32u);
+    if (kSub == 1) {
+      nq = L;
+      d = dlen;
+      return;
+    }
+    const uint32_t s = c.part % kSub, ns = L / 8u;
+    nq = s < ns ? 8u : 0u;
+    d = s + 1 < ns ? 8u * bw : (s + 1 == ns ? dlen - 8u * bw * (ns - 1) : 0u);
+  }
   __device__ static WAgg agg(const WCtx& c) {
-    uint32_t L, bw;
-    frame((c.w >> (8 * c.part)) & 0xFFu, L, bw);
-    return WAgg{L, 32u * ((L * bw + 31u) / 32u), 0u};
+    uint32_t h, nq, bw, d;
+    part(c, h, nq, bw, d);
+    return WAgg{nq, d, 0u};
+  }
+  __device__ static WAgg word_agg_fast(const WCtx& c) {
+    WAgg t{0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint32_t L, bw;
+      frame((c.w >> (8 * k)) & 0xFFu, L, bw);
+      t.q += L;
+      t.d += 32u * ((L * bw + 31u) / 32u);
+    }
+    return t;
   }
   __device__ static bool suspect(const WCtx& c) {  // length code 3 or bit 7
     return ((c.w & (c.w >> 1) & 0x01010101u) | (c.w & 0x80808080u)) != 0;
   }
   template <class F>
   __device__ static void walk(const WCtx& c, F&& f) {
-    const uint32_t h = (c.w >> (8 * c.part)) & 0xFFu;
+    uint32_t h, nq, bw, d;
+    part(c, h, nq, bw, d);
+    if (nq == 0) return;  // (a part past its frame's end)
     Grp g = grp0();
-    frame(h, g.nq, g.bw);
-    g.step = g.bw;
-    g.dlen = 32u * ((g.nq * g.bw + 31u) / 32u);
-    g.err = ((h & 3u) == 3u || (h & 0x80u)) ? GC_DEV_BAD_FRAME : 0u;
+    g.nq = nq;
+    g.bw = bw;
+    g.step = bw;
+    g.dlen = d;
+    g.err = (c.part % kSub == 0 && ((h & 3u) == 3u || (h & 0x80u))) ? GC_DEV_BAD_FRAME : 0u;
     f(g);
   }
 };

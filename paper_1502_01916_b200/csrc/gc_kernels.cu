@@ -136,6 +136,39 @@ __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
 // =====================================================================================
 constexpr uint32_t kLTA = kWA + 2;  // index-kernel list table entries (lists of one tile)
 
+// The group walk of one control word gw (word widx of list l, its groups starting at
+// quad q0, data lane-bit d0, exception byte e0): group codes, and every group of the list
+// inside the list's data / exception range.  Returns status bits.  Out of line: k_index
+// calls it from the walk queue and, when the queue is full, in place.
+struct WalkArgs {  // (by value: a kernel parameter passed by reference would be copied to the stack)
+  const uint32_t* ctrl_words;
+  const uint32_t* list_n;
+  const uint64_t* data_off;
+  const uint64_t* exc_off;
+};
+template <class C>
+__device__ __noinline__ uint32_t index_walk_word(WalkArgs A, uint64_t gw, uint32_t widx, uint64_t l,
+                                                 uint64_t q0, uint64_t d0, uint64_t e0) {
+  uint32_t err = 0;
+  const uint32_t w = A.ctrl_words[gw];
+  const uint32_t pv = (C::kNeedsPrev && widx > 0) ? A.ctrl_words[gw - 1] : 0u;
+  const uint64_t Q = (A.list_n[l] + 3ull) >> 2;
+  const uint64_t dbase = A.data_off[l] * 32ull, dlim = A.data_off[l + 1] * 32ull;
+  const uint64_t elim = A.exc_off ? A.exc_off[l + 1] : 0ull;
+  const WCtx c{w, pv, widx, Q, 0u};
+  word_walk<C>(c, [&](const Grp& g) {
+    const uint64_t gq = q0 + g.q0;
+    if (gq >= Q) return;
+    if (g.err) err |= g.err;
+    if (g.nq == 0) return;
+    const uint64_t gdata = d0 + (int64_t)g.d0;
+    const uint64_t gexc = e0 + g.e0;
+    if (gdata < dbase || gdata + g.dlen > dlim) err |= GC_DEV_TRUNCATED;
+    if (C::kExc && gexc + g.elen > elim) err |= GC_DEV_TRUNCATED;
+  });
+  return err;
+}
+
 #ifndef GC_INDEX_MINB
 #define GC_INDEX_MINB 4
 #endif
@@ -335,27 +368,11 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
 
   // ---- pass 2: absolute positions per word; tile Entries; queue words to walk
   uint32_t err = 0;
-  // group walk of one word: group codes, and every group of the list inside its data /
-  // exception range
+  // group walk of one word (out of line: one copy of the codec's walk in the kernel)
   auto walk_word = [&](uint32_t wr, uint32_t i, uint64_t q0, uint64_t d0, uint64_t e0) {
-    const uint64_t gw = w0 + wr;
-    GC_CHECK(gw < D.n_ctrl_words);
-    const uint32_t w = D.ctrl_words[gw];
-    const uint32_t widx = wr - cw_at(i);
-    const uint32_t pv = (C::kNeedsPrev && widx > 0) ? D.ctrl_words[gw - 1] : 0u;
-    ListCur L;
-    L.load(D, la + i);
-    const WCtx c{w, pv, widx, L.Q, 0u};
-    word_walk<C>(c, [&](const Grp& g) {
-      const uint64_t gq = q0 + g.q0;
-      if (gq >= L.Q) return;
-      if (g.err) err |= g.err;
-      if (g.nq == 0) return;
-      const uint64_t gdata = d0 + (int64_t)g.d0;
-      const uint64_t gexc = e0 + g.e0;
-      if (gdata < L.dbase || gdata + g.dlen > L.dlim) err |= GC_DEV_TRUNCATED;
-      if (C::kExc && gexc + g.elen > L.elim) err |= GC_DEV_TRUNCATED;
-    });
+    GC_CHECK(w0 + wr < D.n_ctrl_words);
+    err |= index_walk_word<C>(WalkArgs{D.ctrl_words, D.list_n, D.data_off, D.exc_off}, w0 + wr,
+                              wr - cw_at(i), la + i, q0, d0, e0);
   };
   uint32_t cq = 0;
   uint64_t cd = 0, ce = 0;

@@ -9,7 +9,7 @@ rm -f profiles/r2_traffic.json.box
 for c in ${CFGS:-1 2 3 4}; do
   case $c in 1) n=1;; 2) n=10;; 3) n=2;; 4) n=1;; esac
   timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    --kernel-name 'regex:k_decode<.*\(bool\)1>|k_index' --launch-count $((3 * n)) \
+    --kernel-name 'regex:k_decode<.*, \(bool\)1, \(bool\)0>|k_index' --launch-count $((3 * n)) \
     -o /tmp/r2_cfg$c -f python bench.py --config $c --steps 1 --warmup 0 --no-e2e \
     --no-cpu-baseline --extra-configs none > gpurun_out/r2/ncu_cfg$c.log 2>&1
   echo "ncu cfg$c rc=$?"
