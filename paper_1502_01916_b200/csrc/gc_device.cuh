@@ -100,7 +100,7 @@ struct WsHeader {
   uint32_t status;
   uint32_t counter_a;
   uint32_t counter_b;
-  uint32_t pad0;
+  uint32_t vb_long;  // Variable Byte: k_varbyte_short saw a list of >= kVbShort ints
   uint32_t pad[12];
   unsigned long long prof[24];  // GC_TIMING builds: cycles per decode phase (debugging aid)
 };
@@ -374,6 +374,60 @@ __device__ __forceinline__ uint32_t lookback_u32(uint64_t* status, uint32_t tile
 #endif
       return acc;
     }
+    base -= 32;
+  }
+}
+
+// Decoupled look-back over TileA slots (the index kernel's control tiles, the Variable Byte
+// byte tiles); one full warp.  Returns in (pq, pd, pe) the sums of the tiles before `tile`
+// back to (and including) the nearest one that published an inclusive prefix.  A slot is
+// published when both of its words carry bit 63 (tilea_pack).
+__device__ __forceinline__ void lookback_tilea(const TileA* tiles, uint32_t tile, uint32_t& pq,
+                                               uint64_t& pd, uint64_t& pe) {
+  const uint32_t lane = threadIdx.x & 31;
+  pq = 0;
+  pd = pe = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    const int64_t idx = base - (int64_t)lane;
+    const TileA* t = tiles + (idx >= 0 ? idx : 0);
+    uint64_t i0 = 1ull << 63, i1 = 1ull << 63, a0 = 0, a1 = 0;  // before tile 0: zero
+    if (idx >= 0) {
+      i0 = ld_relaxed_u64(&t->i0);
+      i1 = ld_relaxed_u64(&t->i1);
+      a0 = ld_relaxed_u64(&t->a0);
+      a1 = ld_relaxed_u64(&t->a1);
+    }
+    uint32_t inclm, first;
+    while (true) {
+      const bool hi = (i0 >> 63) && (i1 >> 63), ha = (a0 >> 63) && (a1 >> 63);
+      const uint32_t valid = __ballot_sync(0xffffffffu, hi || ha);
+      inclm = __ballot_sync(0xffffffffu, hi);
+      first = inclm ? (uint32_t)(__ffs(inclm) - 1) : 31u;
+      const uint32_t need = first == 31u ? 0xffffffffu : ((2u << first) - 1u);
+      if ((valid & need) == need) break;
+      if (!(valid & (1u << lane)) && (need & (1u << lane))) {
+        __nanosleep(32);
+        i0 = ld_relaxed_u64(&t->i0);
+        i1 = ld_relaxed_u64(&t->i1);
+        a0 = ld_relaxed_u64(&t->a0);
+        a1 = ld_relaxed_u64(&t->a1);
+      }
+    }
+    const bool hi = (i0 >> 63) && (i1 >> 63);
+    uint32_t q = 0;
+    uint64_t d = 0, e = 0;
+    if (lane <= first) tilea_unpack(hi ? i0 : a0, hi ? i1 : a1, q, d, e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+      e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    pq += q;
+    pd += d;
+    pe += e;
+    if (inclm) return;
     base -= 32;
   }
 }

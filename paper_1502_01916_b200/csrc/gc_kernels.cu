@@ -308,49 +308,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
     uint32_t pq = 0;
     uint64_t pd = 0, pe = 0;
     if (!first_reset) {
-      int64_t base = (int64_t)tile - 1;
-      while (true) {
-        const int64_t idx = base - (int64_t)lane;
-        const TileA* t = D.tiles_a + (idx >= 0 ? idx : 0);
-        uint64_t i0 = 1ull << 63, i1 = 1ull << 63, a0 = 0, a1 = 0;  // before tile 0: zero
-        if (idx >= 0) {
-          i0 = ld_relaxed_u64(&t->i0);
-          i1 = ld_relaxed_u64(&t->i1);
-          a0 = ld_relaxed_u64(&t->a0);
-          a1 = ld_relaxed_u64(&t->a1);
-        }
-        uint32_t inclm, first;
-        while (true) {
-          const bool hi = (i0 >> 63) && (i1 >> 63), ha = (a0 >> 63) && (a1 >> 63);
-          const uint32_t valid = __ballot_sync(0xffffffffu, hi || ha);
-          inclm = __ballot_sync(0xffffffffu, hi);
-          first = inclm ? (uint32_t)(__ffs(inclm) - 1) : 31u;
-          const uint32_t need = first == 31u ? 0xffffffffu : ((2u << first) - 1u);
-          if ((valid & need) == need) break;
-          if (!(valid & (1u << lane)) && (need & (1u << lane))) {
-            __nanosleep(32);
-            i0 = ld_relaxed_u64(&t->i0);
-            i1 = ld_relaxed_u64(&t->i1);
-            a0 = ld_relaxed_u64(&t->a0);
-            a1 = ld_relaxed_u64(&t->a1);
-          }
-        }
-        const bool hi = (i0 >> 63) && (i1 >> 63);
-        uint32_t q = 0;
-        uint64_t d = 0, e = 0;
-        if (lane <= first) tilea_unpack(hi ? i0 : a0, hi ? i1 : a1, q, d, e);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          q += __shfl_xor_sync(0xffffffffu, q, o);
-          d += __shfl_xor_sync(0xffffffffu, d, o);
-          e += __shfl_xor_sync(0xffffffffu, e, o);
-        }
-        pq += q;
-        pd += d;
-        pe += e;
-        if (inclm) break;
-        base -= 32;
-      }
+      lookback_tilea(D.tiles_a, tile, pq, pd, pe);
       if (tid == 0 && !total.f) {
         uint64_t w0, w1;
         tilea_pack(pq + total.q, pd + total.d, pe + total.e, w0, w1);
@@ -538,11 +496,9 @@ using namespace gcd;
 namespace {
 
 // ------------------------------------------------------------------ Variable Byte
-// The short-list fallback (§7.5; P §2.3): one warp per list reads its bytes 32 at a
-// time; a ballot of the last-byte bits (MSB = 1) ranks the ints, each last byte assembles
-// its int from the (<= 4) bytes before it -- shuffles, and the previous round's last four
-// bytes -- and a warp scan gives the d-gap prefix sum.  Bytes after the list's n ints
-// (the 4-byte padding of the list's area) are ignored.
+// The short-list fallback of P:L640 §7.5 (P §2.3: 7-bit groups, least significant first,
+// MSB = 1 on an int's last byte).  Bytes after a list's n ints (the 4-byte padding of the
+// list's area) are ignored.
 // Short lists (n < kVbShort, the fallback's case): one thread per list, a serial byte loop
 // (staging a warp's 32 lists in shared memory first measured slower).
 constexpr uint32_t kVbShort = 64;
@@ -560,7 +516,7 @@ __device__ __forceinline__ bool vb_list_ok(const Dev& D, uint64_t l, uint32_t n)
 template <bool DGAPS>
 __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restrict__ out) {
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(D.ctrl_words);
-  uint32_t err = 0;
+  uint32_t err = 0, long_seen = 0;
   for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < D.n_lists;
        l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t n = D.list_n[l];
@@ -568,7 +524,12 @@ __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restri
       err |= GC_DEV_TRUNCATED;
       continue;
     }
-    if (n == 0 || n >= kVbShort) continue;
+    if (n >= kVbShort) {
+      if (D.ctrl_off[l + 1] - D.ctrl_off[l] < n) err |= GC_DEV_TRUNCATED;
+      else long_seen = 1u;
+      continue;
+    }
+    if (n == 0) continue;
     const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
     uint64_t p = c0;
     uint32_t acc = 0;
@@ -595,85 +556,298 @@ __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restri
     }
   }
   if (err) atomicOr(&D.hdr->status, err);
+  if (__any_sync(0xffffffffu, long_seen) && (threadIdx.x & 31) == 0) D.hdr->vb_long = 1u;
 }
-template <bool DGAPS>
-__global__ void __launch_bounds__(256) k_varbyte(Dev D, uint32_t* __restrict__ out) {
+// Long lists (n >= kVbShort) in parallel: byte-space tiles of kVbTB bytes (one TileA slot
+// each: the index kernel's control tiles have the same size, so the workspace layout is
+// shared), one CTA per tile, claimed in order.  Each thread holds 32 consecutive bytes; an
+// int ends at a byte with MSB 1 (P §2.3).  A block scan segmented at long-list starts of
+// (ints ended, their sum) and a decoupled look-back across tiles give every int its index in
+// its list and its d-gap prefix.  Bytes of short lists (k_varbyte_short's) and the
+// padding after a list's n ints are skipped.
+constexpr uint32_t kVbTB = 4 * kWA;     // bytes per tile (8192): 32 per thread
+constexpr uint32_t kVbL = 136;          // long lists touching a tile: <= 8192 / 64 + 2
+
+// Largest l in [lo, hi) with off[l] <= key (off non-decreasing, off[lo] <= key); one full
+// warp, 32 probes per step.
+__device__ __forceinline__ uint64_t warp_find(const uint64_t* off, uint64_t lo, uint64_t hi,
+                                              uint64_t key) {
   const uint32_t lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const uint64_t span = hi - lo;
+    const uint64_t p = lo + ((span * (lane + 1)) >> 5);  // non-decreasing in lane; lane 31: hi
+    const bool le = p < hi && off[p] <= key;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);  // a prefix of the lanes
+    const uint64_t nlo = m ? __shfl_sync(0xffffffffu, p, 31 - __clz(m)) : lo;
+    const uint32_t nm = ~m;
+    hi = __shfl_sync(0xffffffffu, p, __ffs(nm) - 1);
+    lo = nlo;
+  }
+  return lo;
+}
+
+template <bool DGAPS>
+__global__ void __launch_bounds__(256) k_varbyte_tiles(Dev D, uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_tile, s_cnt, s_pq, s_pd, s_err;
+  __shared__ unsigned long long s_la, s_lb;
+  __shared__ int32_t s_rs[kVbL];            // list start relative to the tile (>= -8)
+  __shared__ uint32_t s_st[kVbL], s_en[kVbL];  // its bytes in the tile: [st, en)
+  __shared__ uint32_t s_n[kVbL], s_fl[kVbL];   // ints; 1: starts in the tile, 2: ends in it
+  __shared__ unsigned long long s_o[kVbL];
+  __shared__ uint32_t s_wc[8], s_pw[8][2];
+  __shared__ Seg4 s_scr[8];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(D.ctrl_words);
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t err = 0;
-  // warps step over groups of 32 lists, a ballot of the lengths picks the long ones
-  const uint64_t groups = (D.n_lists + 31) / 32;
-  for (uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < groups;
-       g += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-   const uint64_t lg = 32 * g + lane;
-   uint32_t todo = __ballot_sync(0xffffffffu, lg < D.n_lists && D.list_n[lg] >= kVbShort);
-   while (todo) {
-    const uint64_t l = 32 * g + (uint32_t)(__ffs(todo) - 1);
-    todo &= todo - 1;
-    const uint32_t n = D.list_n[l];
-    const uint64_t c0 = D.ctrl_off[l], c1 = D.ctrl_off[l + 1], o0 = D.out_off[l];
-    if (!vb_list_ok(D, l, n)) continue;  // (flagged by k_varbyte_short, which checks every list)
-    uint32_t got = 0, run = 0, carry = 0;  // ints so far, bytes of the open int, d-gap carry
-    uint32_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;  // the previous round's last four bytes
-    for (uint64_t r = c0; r < c1 && got < n; r += 32) {
-      const uint64_t p = r + lane;
-      const uint32_t b = p < c1 ? bytes[p] : 0u;
-      const uint32_t stops = __ballot_sync(0xffffffffu, p < c1 && (b & 128u));
-      const uint32_t before = stops & lt;
-      // bytes of my int before me: since the last stop before me (this round), or the run
-      // carried in from earlier rounds
-      const uint32_t k = before ? lane - (31u - __clz(before)) - 1u : lane + run;
-      const uint32_t s1 = __shfl_up_sync(0xffffffffu, b, 1), s2 = __shfl_up_sync(0xffffffffu, b, 2);
-      const uint32_t s3 = __shfl_up_sync(0xffffffffu, b, 3), s4 = __shfl_up_sync(0xffffffffu, b, 4);
-      const uint32_t prev[5] = {b, lane >= 1 ? s1 : p1, lane >= 2 ? s2 : (lane == 1 ? p1 : p2),
-                                lane >= 3 ? s3 : (lane == 2 ? p1 : (lane == 1 ? p2 : p3)),
-                                lane >= 4 ? s4 : (lane == 3 ? p1 : (lane == 2 ? p2 : (lane == 1 ? p3 : p4)))};
-      uint32_t v = 0;
-      const bool mine = (stops >> lane) & 1u;
-      const uint32_t idx = got + __popc(before);
-      if (mine) {
-        if (k > 4) err |= GC_DEV_BAD_LD;  // more than 5 bytes without a terminator
-        for (uint32_t j = 0; j <= min(k, 4u); j++) v |= (prev[j] & 127u) << (7 * (min(k, 4u) - j));
-      }
-      const bool keep = mine && idx < n;
-      uint32_t inc = keep ? v : 0u;
-      if (DGAPS) {
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= (uint32_t)o) inc += t;
-        }
-      }
-      GC_CHECK(!keep || o0 + idx < D.total_out);
-      if (keep) out[o0 + idx] = DGAPS ? carry + inc : v;
-      if (DGAPS) carry += __shfl_sync(0xffffffffu, inc, 31);
-      got += __popc(stops);
-      const uint32_t last = stops ? 31u - __clz(stops) : 0u;
-      run = stops ? 31u - last : run + 32u;  // bytes after the round's last stop
-      p4 = __shfl_sync(0xffffffffu, b, 28);
-      p3 = __shfl_sync(0xffffffffu, b, 29);
-      p2 = __shfl_sync(0xffffffffu, b, 30);
-      p1 = __shfl_sync(0xffffffffu, b, 31);
+  const uint64_t nbytes = mn64(D.ctrl_off[D.n_lists], 4ull * D.n_ctrl_words);
+  // (stream order: k_varbyte_short has finished; without a long list nothing is left to do)
+  if (*reinterpret_cast<volatile const uint32_t*>(&D.hdr->vb_long) == 0) return;
+  if (tid == 0) {
+    s_tile = atomicAdd(&D.hdr->counter_a, 1u);
+    s_cnt = 0;
+    s_err = 0;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t B0 = (uint64_t)tile * kVbTB;
+  if (warp == 0) {  // lists la..lb overlap [B0, B0 + kVbTB)
+    uint64_t la = 1, lb = 0;
+    if (B0 < nbytes) {
+      la = warp_find(D.ctrl_off, 0, D.n_lists, B0);
+      lb = warp_find(D.ctrl_off, la, D.n_lists, B0 + kVbTB - 1);
     }
-    if (got < n) err |= GC_DEV_TRUNCATED;  // the stream ends before n ints
-   }
+    if (lane == 0) {
+      s_la = la;
+      s_lb = lb;
+    }
+  }
+  __syncthreads();
+  const uint64_t la = s_la, lb = s_lb;
+  // the long lists of the tile, in list order (block compaction, rounds of 256 lists)
+  for (uint64_t r = la; r <= lb && lb >= la; r += 256) {
+    const uint64_t l = r + tid;
+    bool keep = false;
+    uint32_t n = 0;
+    uint64_t c0 = 0, c1 = 0;
+    if (l <= lb) {
+      n = D.list_n[l];
+      if (n >= kVbShort && vb_list_ok(D, l, n)) {
+        c0 = D.ctrl_off[l];
+        c1 = D.ctrl_off[l + 1];
+        // (a list with fewer bytes than ints is flagged by k_varbyte_short and skipped: every
+        // kept list has >= 64 bytes, so at most kVbL of them touch a tile)
+        keep = c1 - c0 >= n && c0 < B0 + kVbTB && c1 > B0;
+      }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_wc[warp] = __popc(m);
+    __syncthreads();
+    uint32_t before = s_cnt;
+    for (uint32_t x = 0; x < warp; x++) before += s_wc[x];
+    if (keep) {
+      const uint32_t k = before + __popc(m & ((1u << lane) - 1u));
+      GC_CHECK(k < kVbL);
+      if (k < kVbL) {
+        const int64_t rs = (int64_t)c0 - (int64_t)B0;
+        s_rs[k] = (int32_t)(rs < -8 ? -8 : rs);
+        s_st[k] = c0 > B0 ? (uint32_t)(c0 - B0) : 0u;
+        s_en[k] = (uint32_t)(mn64(c1, B0 + kVbTB) - B0);
+        s_n[k] = n;
+        s_fl[k] = (c0 >= B0 ? 1u : 0u) | (c1 <= B0 + kVbTB ? 2u : 0u);
+        s_o[k] = D.out_off[l];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = s_cnt;
+      for (uint32_t x = 0; x < 8; x++) t += s_wc[x];
+      if (t > kVbL) s_err |= GC_DEV_TRUNCATED;  // (cannot happen with a consistent directory)
+      s_cnt = min(t, kVbL);
+    }
+    __syncthreads();
+  }
+  const uint32_t cnt = s_cnt;
+  if (cnt == 0) {  // no long list here: an empty inclusive prefix (no list continues through)
+    if (tid == 0) {
+      uint64_t v0, v1;
+      tilea_pack(0, 0, 0, v0, v1);
+      st_relaxed_u64(&D.tiles_a[tile].i1, v1);
+      st_relaxed_u64(&D.tiles_a[tile].i0, v0);
+      if (s_err) atomicOr(&D.hdr->status, s_err);
+    }
+    return;
+  }
+  // my 32 bytes (8 words) and the 8 bytes before them
+  const uint32_t p0 = 32 * tid;
+  const uint64_t g0 = B0 + p0;
+  uint32_t w[8];
+  if (g0 + 32 <= 4ull * D.n_ctrl_words) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(bytes + g0));
+    const uint4 y = __ldg(reinterpret_cast<const uint4*>(bytes + g0) + 1);
+    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; i++) w[i] = g0 + 4 * i + 4 <= 4ull * D.n_ctrl_words ? D.ctrl_words[g0 / 4 + i] : 0u;
+  }
+  if (lane == 31) {
+    s_pw[warp][0] = w[6];
+    s_pw[warp][1] = w[7];
+  }
+  uint32_t pw6 = __shfl_up_sync(0xffffffffu, w[6], 1), pw7 = __shfl_up_sync(0xffffffffu, w[7], 1);
+  __syncthreads();
+  if (lane == 0) {
+    if (warp) {
+      pw6 = s_pw[warp - 1][0];
+      pw7 = s_pw[warp - 1][1];
+    } else {
+      pw6 = B0 >= 8 ? D.ctrl_words[B0 / 4 - 2] : 0u;
+      pw7 = B0 >= 8 ? D.ctrl_words[B0 / 4 - 1] : 0u;
+    }
+  }
+  auto byte_at = [&](uint32_t i) -> uint32_t { return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu; };
+  // the table entry of my first byte: the last list starting at or before it
+  uint32_t k0 = 0;
+  {
+    uint32_t a = 0, b = cnt;
+    while (b - a > 1) {
+      const uint32_t m = (a + b) >> 1;
+      if (s_st[m] <= p0) a = m;
+      else b = m;
+    }
+    k0 = a;
+  }
+  const bool in0 = cnt > 0 && s_st[k0] <= p0 && p0 < s_en[k0];
+  // the open int at my first byte: its bytes among the 8 before me (in its list, after the
+  // last byte with MSB 1)
+  uint32_t cur0 = 0, nb0 = 0;
+  if (in0) {
+    const uint64_t pv = ((uint64_t)pw7 << 32) | pw6;  // bytes p0-8 .. p0-1
+    uint32_t j = 0;
+    while (j < 8) {
+      const int32_t q = (int32_t)p0 - (int32_t)j - 1;
+      const uint32_t b = (uint32_t)(pv >> (8 * (7 - j))) & 0xFFu;
+      if (q < s_rs[k0] || (b & 128u)) break;
+      j++;
+    }
+    nb0 = j;
+    for (uint32_t t = 0; t < min(j, 5u); t++)
+      cur0 |= ((uint32_t)(pv >> (8 * (8 - j + t))) & 127u) << (7 * t);
+  }
+  uint32_t err = 0;
+  // pass 1: (list start seen, ints ended, their sum) of my bytes
+  Seg4 agg{0u, 0u, 0u, 0u};
+  {
+    uint32_t k = k0, cur = cur0, nb = nb0;
+#pragma unroll
+    for (uint32_t i = 0; i < 32; i++) {
+      const uint32_t p = p0 + i;
+      while (k < cnt && p >= s_en[k]) k++;
+      if (k >= cnt || p < s_st[k]) {
+        cur = nb = 0;
+        continue;
+      }
+      if (p == s_st[k] && (s_fl[k] & 1u)) {
+        agg = Seg4{1u, 0u, 0u, 0u};
+        cur = nb = 0;
+      }
+      const uint32_t b = byte_at(i);
+      if (nb < 5) cur |= (b & 127u) << (7 * nb);
+      nb++;
+      if (b & 128u) {
+        if (nb > 5) err |= GC_DEV_BAD_LD;
+        agg.q += 1;
+        agg.d += cur;
+        cur = nb = 0;
+      }
+    }
+  }
+  Seg4 total;
+  const Seg4 excl = block_excl_seg4<false, 8>(agg, s_scr, &total);
+  // the carry into the tile: only if its first bytes continue a long list
+  const bool need_carry = cnt > 0 && s_rs[0] < 0 && s_st[0] == 0 && s_en[0] > 0;
+  if (warp == 0) {
+    TileA* me = D.tiles_a + tile;
+    uint64_t v0, v1;
+    if (!need_carry || total.f) {
+      tilea_pack(total.q, total.d, 0, v0, v1);
+      if (lane == 0) {
+        st_relaxed_u64(&me->i1, v1);
+        st_relaxed_u64(&me->i0, v0);
+      }
+    } else {
+      tilea_pack(total.q, total.d, 0, v0, v1);
+      if (lane == 0) {
+        st_relaxed_u64(&me->a1, v1);
+        st_relaxed_u64(&me->a0, v0);
+      }
+    }
+    uint32_t pq = 0;
+    uint64_t pd = 0, pe = 0;
+    if (need_carry) {
+      lookback_tilea(D.tiles_a, tile, pq, pd, pe);
+      if (lane == 0 && !total.f) {
+        tilea_pack(pq + total.q, (uint32_t)(pd + total.d), 0, v0, v1);
+        st_relaxed_u64(&me->i1, v1);
+        st_relaxed_u64(&me->i0, v0);
+      }
+    }
+    if (lane == 0) {
+      s_pq = pq;
+      s_pd = (uint32_t)pd;
+    }
+  }
+  __syncthreads();
+  // pass 2: every int ended in my bytes to its list position
+  {
+    uint32_t c = excl.f ? excl.q : s_pq + excl.q;
+    uint32_t sum = excl.f ? excl.d : s_pd + excl.d;
+    uint32_t k = k0, cur = cur0, nb = nb0;
+#pragma unroll
+    for (uint32_t i = 0; i < 32; i++) {
+      const uint32_t p = p0 + i;
+      while (k < cnt && p >= s_en[k]) k++;
+      if (k >= cnt || p < s_st[k]) {
+        cur = nb = 0;
+        continue;
+      }
+      if (p == s_st[k] && (s_fl[k] & 1u)) {
+        c = sum = 0;
+        cur = nb = 0;
+      }
+      const uint32_t b = byte_at(i);
+      if (nb < 5) cur |= (b & 127u) << (7 * nb);
+      nb++;
+      if (b & 128u) {
+        sum += cur;
+        if (c < s_n[k]) {
+          GC_CHECK(s_o[k] + c < D.total_out);
+          out[s_o[k] + c] = DGAPS ? sum : cur;
+        }
+        c++;
+        cur = nb = 0;
+      }
+      if (p + 1 == s_en[k] && (s_fl[k] & 2u) && c < s_n[k]) err |= GC_DEV_TRUNCATED;
+    }
   }
   err = __reduce_or_sync(0xffffffffu, err);
-  if (lane == 0 && err) atomicOr(&D.hdr->status, err);
+  if (lane == 0 && err) atomicOr(&s_err, err);
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(&D.hdr->status, s_err);
 }
 
 gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, int stages,
-                         int n_sm) {
+                         int n_sm, bool short_only = false) {
   if (!(stages & GC_STAGE_DECODE)) return GC_OK;
-  const uint64_t blocks = mn64((D.n_lists + 7) / 8, (uint64_t)n_sm * 16);
   const uint64_t sblocks = mn64((D.n_lists + 255) / 256, (uint64_t)n_sm * 16);
+  // byte tiles over the whole stream (tiles without a long list return at once); a
+  // workspace-resetting caller gives them zeroed tickets and look-back slots
+  const uint64_t tiles = (4ull * D.n_ctrl_words + kVbTB - 1) / kVbTB;
   if (dgaps) {
     k_varbyte_short<true><<<(unsigned)mx64(sblocks, 1), 256, 0, st>>>(D, out);
-    k_varbyte<true><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+    if (!short_only && tiles) k_varbyte_tiles<true><<<(unsigned)tiles, 256, 0, st>>>(D, out);
   } else {
     k_varbyte_short<false><<<(unsigned)mx64(sblocks, 1), 256, 0, st>>>(D, out);
-    k_varbyte<false><<<(unsigned)mx64(blocks, 1), 256, 0, st>>>(D, out);
+    if (!short_only && tiles) k_varbyte_tiles<false><<<(unsigned)tiles, 256, 0, st>>>(D, out);
   }
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
@@ -1156,11 +1330,11 @@ gc_status gc_decode_posting_store(const gc_posting_store* s, uint32_t* docs, uin
   if (SD->n_lists && SD->total_out) {
     const WsLayout LS = ws_layout(SD);
     Dev DS = make_dev(SD, w0, LS);
-    st = launch_varbyte(DS, docs + s->short_base, dgaps != 0, cs, GC_STAGE_DECODE, di.n_sm);
+    st = launch_varbyte(DS, docs + s->short_base, dgaps != 0, cs, GC_STAGE_DECODE, di.n_sm, true);
     if (st != GC_OK) return st;
     if (has_tf) {
       Dev DT = make_dev(s->short_tfs, w1, ws_layout(s->short_tfs));
-      st = launch_varbyte(DT, tfs + s->short_base, false, cs, GC_STAGE_DECODE, di.n_sm);
+      st = launch_varbyte(DT, tfs + s->short_base, false, cs, GC_STAGE_DECODE, di.n_sm, true);
     }
   }
   return st;

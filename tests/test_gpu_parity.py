@@ -108,6 +108,37 @@ def test_configs_scaled_all_codecs(k, scale):
         check(w.values, w.list_n, codec, variant, delta=w.delta)
 
 
+def test_varbyte_long_lists_in_parallel():
+    """Variable Byte lists of 64 .. 600k ints (byte-space tiles, the segmented scan and the
+    look-back across tiles): long lists spanning many 8192-byte tiles, lists that start and end
+    mid-tile between short ones, 1..5-byte ints (values up to 2^32-1), both paths, against the
+    oracle; then malformed long lists (a missing terminator run, too few ints)."""
+    rng = np.random.default_rng(64)
+    ln = np.array([600_000, 3, 64, 65, 0, 1, 200_000, 63, 64, 9000, 5, 130_000, 2, 70], np.uint32)
+    ln = np.concatenate([ln, rng.integers(1, 200, 300).astype(np.uint32), np.array([250_000], np.uint32)])
+    bits = rng.integers(1, 33, int(ln.sum()))
+    vals = (rng.integers(0, 1 << 32, int(ln.sum()), dtype=np.uint64) >> (32 - bits).astype(np.uint64))
+    check(vals.astype(np.uint32), ln, O.VARBYTE, 0)
+    # docIDs of one huge list and a few others: the d-gap carry crosses hundreds of tiles
+    ln2 = np.array([1_500_000, 100, 70_000], np.uint32)
+    gaps = rng.geometric(0.02, int(ln2.sum())).astype(np.uint64)
+    docs = np.concatenate([np.cumsum(g) for g in np.split(gaps, np.cumsum(ln2)[:-1])]) % (1 << 32)
+    check(docs.astype(np.uint32), ln2, O.VARBYTE, 0, delta=True)
+    # malformed: a run of 6 bytes without a terminator inside a long list, and a long list cut
+    hb = gc.HostBatch.from_dict(O.encode_batch(vals.astype(np.uint32), ln, O.VARBYTE))
+    hb.ctrl = hb.ctrl.copy()
+    c0 = int(hb.ctrl_off[6])
+    hb.ctrl[c0 + 5000:c0 + 5006] &= 0x7F
+    _, s = gpu_decode(hb, True)
+    assert s & 2
+    hb = gc.HostBatch.from_dict(O.encode_batch(vals.astype(np.uint32), ln, O.VARBYTE))
+    hb.ctrl = hb.ctrl.copy()
+    c0, c1 = int(hb.ctrl_off[11]), int(hb.ctrl_off[12])
+    hb.ctrl[c1 - 40:c1] = 0                               # its last ints never terminate
+    _, s = gpu_decode(hb, True)
+    assert s & (2 | 16)
+
+
 def test_malformed_streams_flagged_not_faulting():
     rng = np.random.default_rng(3)
     w = gen.random_lists(rng, 20, 500, 10)
