@@ -17,10 +17,17 @@ namespace gcd {
 constexpr int kThreads = GC_ITHREADS;  // index / list kernels
 constexpr int kWarps = kThreads / 32;
 
-// Index kernel (control-space tiles): 2048 control words, 8 per thread.
+// Index kernel (control-space tiles): 2048 control words, 8 per thread; batches of fewer
+// than kSmallIndexWords words use 256-word tiles (1 per thread), so a small batch still
+// spreads its control scan over many CTAs (latency, not throughput, bounds it).
 constexpr uint32_t kWA = GC_WA;
 constexpr uint32_t kCA = kWA / kThreads;
 static_assert(kCA == 8, "the index kernel parses 8 control words per thread");
+constexpr uint32_t kWASmall = kThreads;
+#ifndef GC_SMALL_INDEX_WORDS
+#define GC_SMALL_INDEX_WORDS (1u << 20)
+#endif
+constexpr uint64_t kSmallIndexWords = GC_SMALL_INDEX_WORDS;
 
 // Decode kernel (output-space tiles): tile t owns the output ints
 // [t*kT, (t+1)*kT) exactly; it decodes every quadruple that holds one of them.

@@ -44,6 +44,7 @@ struct Dev {
   uint64_t exc_bytes;
   uint64_t total_out;
   uint32_t n_tiles_a, n_tiles_b;
+  uint32_t wa;            // control words per index tile (kWA, or kWASmall for small batches)
   WsHeader* hdr;
   TileA* tiles_a;
   uint64_t* tiles_b;
@@ -94,7 +95,7 @@ __device__ __forceinline__ void report(uint32_t* s_err, uint32_t bits) {
 // k_lists: one thread per list.  Directory consistency (out_off must be the exclusive
 // scan of list_n, offsets monotone and inside the streams, every non-empty list owns at
 // least one control word) and the control-tile map: first_list[a] = 1 + the list owning
-// control word a*kWA (control areas are contiguous and 4-byte aligned).
+// control word a*wa (control areas are contiguous and 4-byte aligned).
 // =====================================================================================
 __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
   uint32_t err = 0;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
       continue;
     }
     const uint64_t w0 = c0 >> 2, w1 = c1 >> 2;
-    for (uint64_t a = (w0 + kWA - 1) / kWA; a * kWA < w1 && a < D.n_tiles_a; a++)
+    for (uint64_t a = (w0 + D.wa - 1) / D.wa; a * D.wa < w1 && a < D.n_tiles_a; a++)
       D.first_list[a] = (uint32_t)(l + 1);
   }
   err = __reduce_or_sync(0xffffffffu, err);
@@ -134,7 +135,6 @@ __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
 // word of every list (and any word a cheap test finds suspicious) is walked group by
 // group to check the list's bounds and the group codes.
 // =====================================================================================
-constexpr uint32_t kLTA = kWA + 2;  // index-kernel list table entries (lists of one tile)
 
 // The group walk of one control word gw (word widx of list l, its groups starting at
 // quad q0, data lane-bit d0, exception byte e0): group codes, and every group of the list
@@ -172,8 +172,10 @@ __device__ __noinline__ uint32_t index_walk_word(WalkArgs A, uint64_t gw, uint32
 #ifndef GC_INDEX_MINB
 #define GC_INDEX_MINB 4
 #endif
-template <class C>
+template <class C, uint32_t CA>
 __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
+  constexpr uint32_t WA = CA * kThreads;  // control words per tile (== D.wa)
+  constexpr uint32_t kLTA = WA + 2;       // list table entries (the lists of one tile)
   __shared__ uint32_t s_cw[kLTA + 1];           // first word of list la+i, relative to w0 (wraps)
   __shared__ uint32_t s_n[kLTA];                // ints of list la+i
   __shared__ unsigned long long s_o[kLTA];      // out_off of list la+i
@@ -190,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
     s_err = 0;
     s_nq = 0;
     s_lastli = 0;
-    const uint64_t w0 = (uint64_t)tile * kWA;
+    const uint64_t w0 = (uint64_t)tile * WA;
     const uint64_t cend = D.n_lists ? mn64(D.ctrl_off[D.n_lists] >> 2, D.n_ctrl_words) : 0;
-    uint64_t nw = cend > w0 ? mn64(kWA, cend - w0) : 0;
+    uint64_t nw = cend > w0 ? mn64(WA, cend - w0) : 0;
     uint64_t la = 0, nl = 0;
     if (nw) {
       const uint32_t f = D.first_list[tile];
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   }
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint64_t w0 = (uint64_t)tile * kWA;
+  const uint64_t w0 = (uint64_t)tile * WA;
   const uint32_t nw = s_nw, nl = s_nl;
   const uint64_t la = s_la;
   const bool big = nl > kLTA;  // (runs of empty lists) look the table up in global memory
@@ -234,19 +236,24 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   auto o_at = [&](uint32_t i) -> uint64_t { return big ? D.out_off[la + i] : s_o[i]; };
 
   // ---- words of this thread (8 consecutive, two 128-bit loads)
-  const uint32_t r0 = tid * kCA;
-  const uint32_t myn = r0 < nw ? min(kCA, nw - r0) : 0u;
-  uint32_t wv[kCA];
-  if (myn == kCA) {
-    const uint4 x = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0));
-    const uint4 y = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0) + 1);
-    wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
-    wv[4] = y.x; wv[5] = y.y; wv[6] = y.z; wv[7] = y.w;
+  const uint32_t r0 = tid * CA;
+  const uint32_t myn = r0 < nw ? min(CA, nw - r0) : 0u;
+  uint32_t wv[CA];
+  if constexpr (CA == 8) {
+    if (myn == CA) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0));
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(D.ctrl_words + w0 + r0) + 1);
+      wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
+      wv[4] = y.x; wv[5] = y.y; wv[6] = y.z; wv[7] = y.w;
+    } else {
+#pragma unroll
+      for (uint32_t k = 0; k < CA; k++) wv[k] = k < myn ? D.ctrl_words[w0 + r0 + k] : 0u;
+    }
   } else {
 #pragma unroll
-    for (uint32_t k = 0; k < kCA; k++) wv[k] = k < myn ? D.ctrl_words[w0 + r0 + k] : 0u;
+    for (uint32_t k = 0; k < CA; k++) wv[k] = k < myn ? D.ctrl_words[w0 + r0 + k] : 0u;
   }
-  uint32_t pw = __shfl_up_sync(0xffffffffu, wv[kCA - 1], 1);
+  uint32_t pw = __shfl_up_sync(0xffffffffu, wv[CA - 1], 1);
   if (lane == 0) pw = (C::kNeedsPrev && myn && w0 + r0 > 0) ? D.ctrl_words[w0 + r0 - 1] : 0u;
 
   uint32_t li = 0;
@@ -261,10 +268,10 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   }
   // pass 1: per-word aggregates, segmented at list starts
   Seg4 agg{0, 0, 0, 0};
-  WAgg wa_[kCA];
-  uint32_t wli[kCA];
+  WAgg wa_[CA];
+  uint32_t wli[CA];
 #pragma unroll
-  for (uint32_t k = 0; k < kCA; k++) {
+  for (uint32_t k = 0; k < CA; k++) {
     wa_[k] = WAgg{0, 0, 0};
     wli[k] = li;
     if (k < myn) {
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   uint32_t ci = ~0u, c_cw = 0, c_cwn = 0, c_n = 0;
   uint64_t c_o = 0;
 #pragma unroll
-  for (uint32_t k = 0; k < kCA; k++) {
+  for (uint32_t k = 0; k < CA; k++) {
     if (k >= myn) break;
     const uint32_t wr = r0 + k;
     const uint32_t i = wli[k];
@@ -853,14 +860,21 @@ gc_status launch_varbyte(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t s
 }
 
 struct WsLayout {
-  uint64_t n_tiles_a, n_tiles_b;
+  uint64_t n_tiles_a, n_tiles_b, wa;
   uint64_t off_tiles_a, off_tiles_b, off_entries, off_first, bytes;
 };
 
 WsLayout ws_layout(const gc_batch* b) {
   WsLayout L;
   uint64_t words = b->ctrl_bytes / 4;
-  L.n_tiles_a = (words + kWA - 1) / kWA;
+  L.wa = words < kSmallIndexWords ? kWASmall : kWA;
+  // GC_INDEX_TILE_WORDS=256|2048 forces one index tile size (a test knob; the workspace size
+  // and the decode must see the same setting)
+  if (const char* e = getenv("GC_INDEX_TILE_WORDS")) {
+    const uint64_t v = strtoull(e, nullptr, 10);
+    if (v == kWASmall || v == kWA) L.wa = v;
+  }
+  L.n_tiles_a = (words + L.wa - 1) / L.wa;
   if (L.n_tiles_a == 0) L.n_tiles_a = 1;
   L.n_tiles_b = (b->total_out + kT - 1) / kT;
   L.off_tiles_a = sizeof(WsHeader);
@@ -936,7 +950,8 @@ gc_status launch_index(const Dev& D, cudaStream_t st, const DevInfo& di) {
   const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
   k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)di.n_sm * 8), kThreads, 0, st>>>(D);
   if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-  k_index<C><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+  if (D.wa == kWA) k_index<C, kCA><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+  else k_index<C, 1><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
 
@@ -1008,6 +1023,7 @@ Dev make_dev(const gc_batch* b, uint8_t* w, const WsLayout& L) {
   D.exc_bytes = b->exc_bytes;
   D.total_out = b->total_out;
   D.n_tiles_a = (uint32_t)L.n_tiles_a;
+  D.wa = (uint32_t)L.wa;
   D.n_tiles_b = (uint32_t)L.n_tiles_b;
   D.hdr = (WsHeader*)w;
   D.tiles_a = (TileA*)(w + L.off_tiles_a);

@@ -69,6 +69,19 @@ def test_random_ragged(codec, variant):
         check(w.values, w.list_n, codec, variant)
 
 
+@pytest.mark.parametrize("tile_words", ["256", "2048"])
+@pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
+def test_both_index_tile_sizes(codec, variant, tile_words, monkeypatch):
+    """The index stage's two control-tile sizes (256 words for small batches, 2048 otherwise)
+    forced on the same ragged batches (lists from 1 int to 60k, runs of empty lists)."""
+    monkeypatch.setenv("GC_INDEX_TILE_WORDS", tile_words)
+    rng = np.random.default_rng(77 + codec + 16 * variant)
+    w = gen.random_lists(rng, 120, 60000, 18, 0.02)
+    ln = np.concatenate([w.list_n, np.zeros(700, np.uint32), np.array([1, 2, 3], np.uint32)])
+    vals = np.concatenate([w.values, rng.integers(0, 1 << 10, 6).astype(np.uint32)])
+    check(vals, ln, codec, variant)
+
+
 @pytest.mark.parametrize("codec,variant", CODECS, ids=IDS)
 def test_edge_shapes(codec, variant):
     """Empty lists, 1-int lists (thousands of lists per tile: control/data staging falls
