@@ -158,7 +158,7 @@ gc_status gc_decode_dgaps(const gc_batch* b, uint32_t* out, void* ws, uint64_t w
  * The decode stage is one cooperative launch of min(tiles, SMs x resident CTAs) CTAs, each
  * taking every grid-th 8192-int tile; the environment variable GC_DECODE_MAX_GRID, if set,
  * caps that grid (a test knob: many tiles per CTA at small sizes; same results).  The index
- * stage scans control tiles of 2048 words, or of 256 words for batches under 2^20 control
+ * stage scans control tiles of 2048 words, or of 256 words for batches under 2^18 control
  * words (more CTAs for a small batch); GC_INDEX_TILE_WORDS=256|2048 forces one size (a test
  * knob: it changes gc_workspace_size too, so set it before sizing the workspace). */
 enum { GC_STAGE_RESET = 1, GC_STAGE_INDEX = 2, GC_STAGE_DECODE = 4, GC_STAGE_ALL = 7 };

@@ -25,7 +25,7 @@ constexpr uint32_t kCA = kWA / kThreads;
 static_assert(kCA == 8, "the index kernel parses 8 control words per thread");
 constexpr uint32_t kWASmall = kThreads;
 #ifndef GC_SMALL_INDEX_WORDS
-#define GC_SMALL_INDEX_WORDS (1u << 20)
+#define GC_SMALL_INDEX_WORDS (1u << 18)
 #endif
 constexpr uint64_t kSmallIndexWords = GC_SMALL_INDEX_WORDS;
 

@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kThreads) k_lists(Dev D) {
       continue;
     }
     const uint64_t w0 = c0 >> 2, w1 = c1 >> 2;
-    for (uint64_t a = (w0 + D.wa - 1) / D.wa; a * D.wa < w1 && a < D.n_tiles_a; a++)
+    const uint32_t sh = D.wa == kWA ? 11u : 8u;  // log2 of the tile size (no 64-bit division)
+    static_assert(kWA == 2048u && kWASmall == 256u, "tile sizes");
+    for (uint64_t a = (w0 + D.wa - 1) >> sh; (a << sh) < w1 && a < D.n_tiles_a; a++)
       D.first_list[a] = (uint32_t)(l + 1);
   }
   err = __reduce_or_sync(0xffffffffu, err);
@@ -172,7 +174,9 @@ __device__ __noinline__ uint32_t index_walk_word(WalkArgs A, uint64_t gw, uint32
 #ifndef GC_INDEX_MINB
 #define GC_INDEX_MINB 4
 #endif
-template <class C, uint32_t CA>
+// SKIP: also write the skip entries (gc_build_skip); the decode path's instantiation has
+// none of that code (it cost the decode's index stage ~10% in registers and issue).
+template <class C, uint32_t CA, bool SKIP>
 __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   constexpr uint32_t WA = CA * kThreads;  // control words per tile (== D.wa)
   constexpr uint32_t kLTA = WA + 2;       // list table entries (the lists of one tile)
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
         D.entries[t] = e;
       }
     }
-    if (D.skip && n > 0) {
+    if (SKIP && n > 0) {
       // skip pointers (§7.5): this word owns the first quad 128b of blocks b
       // with 128b in [cq, cq + a.q), b < ceil(n / 512)
       const uint64_t nblk = (n + GC_SKIP_DIST - 1) / GC_SKIP_DIST;
@@ -950,8 +954,14 @@ gc_status launch_index(const Dev& D, cudaStream_t st, const DevInfo& di) {
   const uint64_t lb = (D.n_lists + kThreads - 1) / kThreads;
   k_lists<<<(unsigned)mn64(mx64(lb, 1), (uint64_t)di.n_sm * 8), kThreads, 0, st>>>(D);
   if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
-  if (D.wa == kWA) k_index<C, kCA><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
-  else k_index<C, 1><<<(unsigned)D.n_tiles_a, kThreads, 0, st>>>(D);
+  const dim3 g((unsigned)D.n_tiles_a);
+  if (D.skip) {
+    if (D.wa == kWA) k_index<C, kCA, true><<<g, kThreads, 0, st>>>(D);
+    else k_index<C, 1, true><<<g, kThreads, 0, st>>>(D);
+  } else {
+    if (D.wa == kWA) k_index<C, kCA, false><<<g, kThreads, 0, st>>>(D);
+    else k_index<C, 1, false><<<g, kThreads, 0, st>>>(D);
+  }
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
 
