@@ -439,6 +439,24 @@ __device__ __forceinline__ void lookback_tilea(const TileA* tiles, uint32_t tile
   }
 }
 
+// Largest l in [lo, hi) with off[l] <= key (off non-decreasing, off[lo] <= key); one full
+// warp, 32 probes per step.
+__device__ __forceinline__ uint64_t warp_find(const uint64_t* off, uint64_t lo, uint64_t hi,
+                                              uint64_t key) {
+  const uint32_t lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const uint64_t span = hi - lo;
+    const uint64_t p = lo + ((span * (lane + 1)) >> 5);  // non-decreasing in lane; lane 31: hi
+    const bool le = p < hi && off[p] <= key;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);  // a prefix of the lanes
+    const uint64_t nlo = m ? __shfl_sync(0xffffffffu, p, 31 - __clz(m)) : lo;
+    const uint32_t nm = ~m;
+    hi = __shfl_sync(0xffffffffu, p, __ffs(nm) - 1);
+    lo = nlo;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ uint32_t mask_bits(uint32_t b) {
   return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
 }

@@ -579,24 +579,6 @@ __global__ void __launch_bounds__(256) k_varbyte_short(Dev D, uint32_t* __restri
 constexpr uint32_t kVbTB = 4 * kWA;     // bytes per tile (8192): 32 per thread
 constexpr uint32_t kVbL = 136;          // long lists touching a tile: <= 8192 / 64 + 2
 
-// Largest l in [lo, hi) with off[l] <= key (off non-decreasing, off[lo] <= key); one full
-// warp, 32 probes per step.
-__device__ __forceinline__ uint64_t warp_find(const uint64_t* off, uint64_t lo, uint64_t hi,
-                                              uint64_t key) {
-  const uint32_t lane = threadIdx.x & 31;
-  while (hi - lo > 1) {
-    const uint64_t span = hi - lo;
-    const uint64_t p = lo + ((span * (lane + 1)) >> 5);  // non-decreasing in lane; lane 31: hi
-    const bool le = p < hi && off[p] <= key;
-    const uint32_t m = __ballot_sync(0xffffffffu, le);  // a prefix of the lanes
-    const uint64_t nlo = m ? __shfl_sync(0xffffffffu, p, 31 - __clz(m)) : lo;
-    const uint32_t nm = ~m;
-    hi = __shfl_sync(0xffffffffu, p, __ffs(nm) - 1);
-    lo = nlo;
-  }
-  return lo;
-}
-
 template <bool DGAPS>
 __global__ void __launch_bounds__(256) k_varbyte_tiles(Dev D, uint32_t* __restrict__ out) {
   __shared__ uint32_t s_tile, s_cnt, s_pq, s_pd, s_err;
@@ -1067,7 +1049,7 @@ gc_status run_codec(const Dev& D, uint32_t* out, const Job& J, cudaStream_t st, 
   }
   // JOB_RANGE: the covering entries, then one warp per 512-int block
   unsigned long long* eb = reinterpret_cast<unsigned long long*>(D.hdr->prof);
-  k_range_bounds<<<1, 1, 0, st>>>(D, J.first, J.last, eb);
+  k_range_bounds<<<1, 32, 0, st>>>(D, J.first, J.last, eb);
   if (cudaGetLastError() != cudaSuccess) return GC_ERR_CUDA;
   const uint64_t blocks = (J.last - J.first) / GC_SKIP_DIST + 2 * 32;  // (a bound of the count)
   const unsigned grid = (unsigned)mn64((blocks + kRangeW - 1) / kRangeW + 1, (uint64_t)di.n_sm * 16);
@@ -1095,8 +1077,12 @@ gc_status decode_impl(const gc_batch* b, uint32_t* out, void* ws, uint64_t ws_by
   if (s != GC_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* w = (uint8_t*)ws;
+  // (a range decode's status word is reset by k_range_bounds, its first kernel: one stream
+  // operation fewer on the random-access path; an empty range still gets the memset)
+  const bool range_kernels = J.kind == JOB_RANGE && b->n_lists && b->total_out && J.last > J.first;
   const uint64_t reset = J.kind == JOB_RANGE ? kRangeWsBytes : L.bytes;
-  if ((J.kind != JOB_DECODE || (J.stages & GC_STAGE_RESET)) && cudaMemsetAsync(ws, 0, reset, st) != cudaSuccess)
+  if (!range_kernels && (J.kind != JOB_DECODE || (J.stages & GC_STAGE_RESET)) &&
+      cudaMemsetAsync(ws, 0, reset, st) != cudaSuccess)
     return GC_ERR_CUDA;
   if (J.kind == JOB_SKIP && b->n_lists == 0)
     return cudaMemsetAsync(skip_off_out, 0, 8, st) == cudaSuccess ? GC_OK : GC_ERR_CUDA;

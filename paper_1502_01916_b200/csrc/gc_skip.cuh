@@ -38,20 +38,17 @@ __global__ void __launch_bounds__(kSkipT) k_skip_off(Dev D) {
   if (tid == 0) D.skip_off[D.n_lists] = carry;
 }
 
-// The entry range [e0, e1) covering output ints [first, last): one thread.
+// The entry range [e0, e1) covering output ints [first, last): one warp (32-ary searches,
+// a few dependent loads instead of log2(lists)).
 __global__ void k_range_bounds(Dev D, uint64_t first, uint64_t last, unsigned long long* eb) {
-  auto list_of = [&](uint64_t p) {  // the list holding output int p (the last such)
-    uint64_t a = 0, b = D.n_lists;
-    while (b - a > 1) {
-      const uint64_t m = (a + b) >> 1;
-      if (D.out_off[m] <= p) a = m;
-      else b = m;
-    }
-    return a;
-  };
-  const uint64_t la = list_of(first), lb = list_of(last - 1);
-  eb[0] = D.skip_off[la] + (first - D.out_off[la]) / GC_SKIP_DIST;
-  eb[1] = D.skip_off[lb] + (last - 1 - D.out_off[lb]) / GC_SKIP_DIST + 1;
+  // the list holding output int p: the last l with out_off[l] <= p
+  const uint64_t la = warp_find(D.out_off, 0, D.n_lists, first);
+  const uint64_t lb = warp_find(D.out_off, la, D.n_lists, last - 1);
+  if (threadIdx.x == 0) {
+    D.hdr->status = 0u;  // (the call's status reset: k_range runs after this kernel)
+    eb[0] = D.skip_off[la] + (first - D.out_off[la]) / GC_SKIP_DIST;
+    eb[1] = D.skip_off[lb] + (last - 1 - D.out_off[lb]) / GC_SKIP_DIST + 1;
+  }
 }
 
 constexpr uint32_t kRangeW = 4;  // warps per CTA of k_range
@@ -66,15 +63,13 @@ __global__ void __launch_bounds__(32 * kRangeW) k_range(Dev D, uint32_t* __restr
   constexpr uint32_t FULL = 0xffffffffu;
   const uint64_t e0 = eb[0], e1 = eb[1];
   uint32_t err = 0;
+  uint64_t lc = ~0ull;  // the list of the warp's previous block
   for (uint64_t e = e0 + (uint64_t)blockIdx.x * kRangeW + wl; e < e1; e += (uint64_t)gridDim.x * kRangeW) {
-    // the block's list: skip_off[l] <= e < skip_off[l + 1]
-    uint64_t a = 0, b = D.n_lists;
-    while (b - a > 1) {
-      const uint64_t m = (a + b) >> 1;
-      if (D.skip_off[m] <= e) a = m;
-      else b = m;
-    }
-    const uint64_t l = a;
+    // the block's list: skip_off[l] <= e < skip_off[l + 1] (a warp-wide 32-ary search,
+    // starting from the previous block's list when it still holds this one)
+    if (!(lc < D.n_lists && D.skip_off[lc] <= e && e < D.skip_off[lc + 1]))
+      lc = warp_find(D.skip_off, lc < D.n_lists && D.skip_off[lc] <= e ? lc : 0, D.n_lists, e);
+    const uint64_t l = lc;
     const uint64_t blk = e - D.skip_off[l];
     const uint32_t n = D.list_n[l];
     const uint64_t Q = (n + 3ull) >> 2, nblk = (n + GC_SKIP_DIST - 1) / GC_SKIP_DIST;
