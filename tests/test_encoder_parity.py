@@ -89,3 +89,35 @@ def test_posting_store_short_lists_are_varbyte():
     for i in range(len(w.list_n)):
         o, n = int(st.list_out_off[i]), int(w.list_n[i])
         assert np.array_equal(out[o:o + n], w.values[starts[i]:starts[i] + n]), i
+
+
+@pytest.mark.parametrize("lengths", [[0], [63], [64], [63, 64, 0, 1, 200, 0], [5] * 40,
+                                     [100, 65, 64], []])
+def test_posting_split_edges(lengths):
+    """gc_posting_split / gc_posting_gather on the threshold (63 short, 64 long), empty
+    lists, an all-short and an all-long store, no lists at all: every list (docIDs and TFs)
+    is found at list_out_off after an oracle decode of both groups; short_base is 16-byte
+    aligned and after the long group."""
+    rng = np.random.default_rng(len(lengths))
+    ln = np.array(lengths, np.uint32)
+    n = int(ln.sum())
+    vals = np.zeros(n, np.uint32)
+    starts = np.concatenate([[0], np.cumsum(ln.astype(np.int64))[:-1]]) if len(ln) else np.zeros(0, np.int64)
+    for i, k in enumerate(ln.tolist()):
+        vals[starts[i]:starts[i] + k] = np.cumsum(rng.integers(1, 1000, k)).astype(np.uint32)
+    tfs = rng.integers(0, 300, n).astype(np.uint32)
+    st = gc.encode_posting_store(vals, ln, O.GROUP_AFOR, 0, delta=True, tfs=tfs)
+    assert st.short_base % 4 == 0 and st.short_base >= st.long.total_out
+    assert np.all(st.short.list_n < 64) and np.all(st.long.list_n >= 64)
+    docs = np.zeros(max(st.total, 1), np.uint32)
+    tf = np.zeros(max(st.total, 1), np.uint32)
+    if st.long.total_out:
+        docs[:st.long.total_out] = O.decode_batch(st.long.as_dict(), dgaps=True)
+        tf[:st.long.total_out] = O.decode_batch(st.tf_long.as_dict(), dgaps=False)
+    if st.short.total_out:
+        docs[st.short_base:st.short_base + st.short.total_out] = O.decode_batch(st.short.as_dict(), dgaps=True)
+        tf[st.short_base:st.short_base + st.short.total_out] = O.decode_batch(st.tf_short.as_dict(), dgaps=False)
+    for i, k in enumerate(ln.tolist()):
+        o = int(st.list_out_off[i])
+        assert np.array_equal(docs[o:o + k], vals[starts[i]:starts[i] + k]), i
+        assert np.array_equal(tf[o:o + k], tfs[starts[i]:starts[i] + k]), i
