@@ -14,8 +14,9 @@ import sys
 from collections import defaultdict
 
 
-def launches(path, only="gcd::"):
+def launches(path, only="k_"):
     rows = [r for r in csv.reader(open(path)) if r and r[0] not in ("==PROF==",) and not r[0].startswith("==")]
+    rows = rows[next(i for i, r in enumerate(rows) if r[0] == "ID"):]  # (ncu notes before the header)
     hdr = rows[0]
     idx = {h: i for i, h in enumerate(hdr)}
     tot = defaultdict(float)
