@@ -22,6 +22,9 @@
 #ifndef GC_AFOR_SUB
 #define GC_AFOR_SUB 1  // Group-AFOR parse units per frame header (4: 8-quad parts, measured 6% slower)
 #endif
+#ifndef GC_AFOR_SPLIT
+#define GC_AFOR_SPLIT 1
+#endif
 #ifndef GC_FRAME_UPT
 #define GC_FRAME_UPT 2  // parse units per thread per chunk for the frame codecs (AFOR, PFD)
 #endif
@@ -416,6 +419,7 @@ struct CodecAFOR {
   static constexpr bool kNeedsPrev = false;
   static constexpr bool kMultiQuad = true;
   static constexpr bool kVectorGroups = true;
+  static constexpr bool kSplitPieces = GC_AFOR_SPLIT != 0;  // decode: frames queued in 8-quad pieces
   __device__ static __forceinline__ void frame(uint32_t h, uint32_t& L, uint32_t& bw) {
     L = (h & 3u) == 3u ? 8u : (8u << (h & 3u));
     bw = ((h >> 2) & 31u) + 1u;

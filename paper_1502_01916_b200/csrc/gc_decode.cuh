@@ -99,6 +99,22 @@ struct UnitsPerThread<C, std::void_t<decltype(C::kUnitsPerThread)>> {
   static constexpr uint32_t v = C::kUnitsPerThread;
 };
 
+// Work split for codecs with long multi-quad groups (Group-AFOR frames of 8..32 quads, one
+// parse unit each): a unit's thread unpacks the first kPiece quads of its frame and queues
+// the rest as kPiece-quad pieces, which every thread then takes round-robin -- the lanes of
+// a warp no longer wait for the one holding a 32-quad frame (ncu: 12 of 32 lanes active in
+// the unpack loop without it).
+template <class C, class = void>
+struct SplitPieces {
+  static constexpr bool v = false;
+};
+template <class C>
+struct SplitPieces<C, std::void_t<decltype(C::kSplitPieces)>> {
+  static constexpr bool v = C::kSplitPieces;
+};
+constexpr uint32_t kPiece = 8;     // quads per queued piece
+constexpr uint32_t kPQ = 320;      // queue capacity (a tile holds <= ~2050 quads)
+
 #ifndef GC_DECODE_MINB
 #define GC_DECODE_MINB 3
 #endif
@@ -162,13 +178,18 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
   auto setup = [&](uint32_t vt, uint32_t buf) {
     const Dev& D = bat(vt);
     const uint32_t tile = tix(vt);
-    const uint64_t cend = D.ctrl_off[D.n_lists] >> 2;   // end of the last list's control
-    const uint64_t dend = D.data_off[D.n_lists];
-    const uint64_t eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
     Geo& g = s_g[buf];
     const Entry& E0 = s_e[0];
     const Entry& E1 = s_e[1];
     const bool last = tile + 1 == D.n_tiles_b;
+    // the batch's stream ends bound only the last tile: read them there alone (thread 0's
+    // global round trip would otherwise sit in every tile's path to the next barrier)
+    uint64_t cend = 0, dend = 0, eend = 0;
+    if (last && vt < nvt) {
+      cend = D.ctrl_off[D.n_lists] >> 2;  // end of the last list's control
+      dend = D.data_off[D.n_lists];
+      eend = C::kExc ? D.exc_off[D.n_lists] : 0ull;
+    }
     g.ok = 0;
     uint32_t cbytes = 0, xbytes = 0, dbytes = 0;
     if (vt < nvt) {
@@ -222,6 +243,10 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
     uint64_t tT;
   };
   __shared__ Pend s_pend;
+  constexpr bool kSplit = SplitPieces<C>::v;
+  // piece = (data lane-bit of its first quad, idx[13:0] | rem[19:14] | cnt[23:20] | bw[29:24])
+  __shared__ uint2 s_pq[kSplit ? kPQ : 1];
+  __shared__ uint32_t s_qn;
   auto flush_pending = [&]() {  // all threads; s_pend.on was read after a barrier
     if (warp == 0) {
 #ifdef GC_ABL_NOLB
@@ -289,6 +314,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
   if (tid == 0) {
     s_reset0[0] = kT;
     s_pend.on = 0;
+    s_qn = 0;
   }
   __syncthreads();
   if (tid == 0) setup(first_tile, 0);
@@ -486,7 +512,25 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
                   const uint32_t ja = max(gq, qa), jb = min(gq + g.nq, qb);
                   if (ja >= jb) return;
                   const uint32_t gd = SW.d + (uint32_t)g.d0;
-                  for (uint32_t j = ja; j < jb; j++)
+                  uint32_t jend = jb;
+                  if constexpr (kSplit) {
+                    if (jb - ja > kPiece) {
+                      jend = ja + kPiece;
+                      for (uint32_t p = jend; p < jb; p += kPiece) {
+                        const uint32_t cnt = min(kPiece, jb - p);
+                        const uint32_t pos = gd + (p - gq) * g.step, idx = oref + 4u * p;
+                        const uint32_t slot = idx < (1u << 14) ? atomicAdd(&s_qn, 1u) : kPQ;
+                        if (slot < kPQ) {
+                          s_pq[slot] = make_uint2(pos, idx | (min(n - 4u * p, 32u) << 14) | (cnt << 20) |
+                                                           (g.bw << 24));
+                        } else {
+                          for (uint32_t j = p; j < p + cnt; j++)
+                            unpack_quad(gd + (j - gq) * g.step, g.bw, oref + 4u * j, n - 4u * j, staged);
+                        }
+                      }
+                    }
+                  }
+                  for (uint32_t j = ja; j < jend; j++)
                     unpack_quad(gd + (j - gq) * g.step, g.bw, oref + 4u * j, n - 4u * j, staged);
                   if constexpr (C::kExc) {
                     // Group-PFD: the frame's exceptions in this unit's quads overwrite their
@@ -540,10 +584,27 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
     if (!w0done) mbar_wait(&s_bar[0], phase);
     if (!w1done) mbar_wait(&s_bar[1], phase);
     phase ^= 1u;
+    if constexpr (kSplit) {
+      __syncthreads();  // every unit has queued its pieces
+      const uint32_t nq = min(s_qn, kPQ);
+      auto pieces = [&](auto staged) {
+        for (uint32_t x = tid; x < nq; x += kDT) {
+          const uint2 pc = s_pq[x];
+          const uint32_t idx = pc.y & 0x3FFFu, rem = (pc.y >> 14) & 63u;
+          const uint32_t cnt = (pc.y >> 20) & 15u, bw = pc.y >> 24;
+          for (uint32_t k = 0; k < cnt; k++) unpack_quad(pc.x + k * bw, bw, idx + 4u * k, rem - 4u * k, staged);
+        }
+      };
+      if (data_st) pieces(std::true_type{});
+      else pieces(std::false_type{});
+    }
     if (DGAPS && s_pend.on) flush_pending();  // (a tile that staged nothing)
     __syncthreads();  // the tile is staged; the staging buffers and the next entries are free
     // the next tile's copies overlap this tile's scan, look-back and stores
-    if (tid == 0) setup(vt + gridDim.x, buf ^ 1u);
+    if (tid == 0) {
+      setup(vt + gridDim.x, buf ^ 1u);
+      if (kSplit) s_qn = 0;  // (every thread read it before the barrier above)
+    }
     GC_T(4);
 
     // ------------------------------------------------------------------ d-gap scan

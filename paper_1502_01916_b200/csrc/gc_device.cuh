@@ -231,10 +231,48 @@ __device__ __forceinline__ Seg4 warp_incl_seg4(Seg4 inc, uint32_t lane, uint32_t
   }
   return inc;
 }
+// Without exceptions the flag rides in bit 31 of q (a segment's raw quads stay < 2^31):
+// (f<<31 | q, d), two shuffles per step instead of three, and b (+) ... keeps b's word
+// when its flag is set, else adds (b has no flag bit, so a's flag survives the add).
+#ifndef GC_SEG_PACK
+#define GC_SEG_PACK 1
+#endif
+__device__ __forceinline__ uint2 warp_incl_seg2(uint2 inc, uint32_t lane, uint32_t width) {
+#pragma unroll
+  for (uint32_t o = 1; o < 32; o <<= 1) {
+    if (o >= width) break;
+    const uint32_t nx = __shfl_up_sync(0xffffffffu, inc.x, o);
+    const uint32_t ny = __shfl_up_sync(0xffffffffu, inc.y, o);
+    if (lane >= o && !(inc.x >> 31)) {
+      inc.x += nx;
+      inc.y += ny;
+    }
+  }
+  return inc;
+}
+
 // Exclusive segmented scan; returns this thread's prefix, *total = the block aggregate.
 template <bool kExc, uint32_t NW = kWarps>
 __device__ __forceinline__ Seg4 block_excl_seg4(Seg4 v, Seg4* scratch, Seg4* total) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (!kExc && GC_SEG_PACK) {
+    uint2* scr = reinterpret_cast<uint2*>(scratch);
+    const uint2 inc = warp_incl_seg2(make_uint2(v.q | (v.f ? 0x80000000u : 0u), v.d), lane, 32);
+    if (lane == 31) scr[warp] = inc;
+    uint2 ex = make_uint2(__shfl_up_sync(0xffffffffu, inc.x, 1), __shfl_up_sync(0xffffffffu, inc.y, 1));
+    if (lane == 0) ex = make_uint2(0u, 0u);
+    __syncthreads();
+    uint2 w = lane < NW ? scr[lane] : make_uint2(0u, 0u);
+    w = warp_incl_seg2(w, lane, NW);
+    const uint32_t src = warp ? warp - 1 : 0;
+    uint2 wpre = make_uint2(__shfl_sync(0xffffffffu, w.x, src), __shfl_sync(0xffffffffu, w.y, src));
+    if (warp == 0) wpre = make_uint2(0u, 0u);
+    const uint32_t tx = __shfl_sync(0xffffffffu, w.x, NW - 1), ty = __shfl_sync(0xffffffffu, w.y, NW - 1);
+    *total = Seg4{tx >> 31, tx & 0x7FFFFFFFu, ty, 0u};
+    __syncthreads();
+    const uint2 r = (ex.x >> 31) ? ex : make_uint2(wpre.x + ex.x, wpre.y + ex.y);
+    return Seg4{r.x >> 31, r.x & 0x7FFFFFFFu, r.y, 0u};
+  }
   const Seg4 inc = warp_incl_seg4<kExc>(v, lane, 32);
   if (lane == 31) scratch[warp] = inc;
   Seg4 ex;
