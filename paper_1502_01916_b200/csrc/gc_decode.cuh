@@ -38,6 +38,12 @@ struct Caps<C, std::void_t<decltype(C::kFrameQuads)>> {
   static constexpr uint32_t ccap = 256;
   static constexpr uint32_t dcap = kDCap + (kCCap - ccap) * 4 / 16 + (C::kExc ? 0u : kECap / 16);
 };
+// Group-AFOR: one header byte per 8..32-quad frame, so a tile needs ~64 control words (plus
+// one per list start): 512 staged words leave room for the piece queue.
+template <>
+struct Caps<CodecAFOR, void> {
+  static constexpr uint32_t ccap = 512, dcap = kDCap;
+};
 template <class C>
 struct DS {  // dynamic shared memory layout (byte offsets)
   static constexpr uint32_t kCC = Caps<C>::ccap, kDC = Caps<C>::dcap;
@@ -112,8 +118,11 @@ template <class C>
 struct SplitPieces<C, std::void_t<decltype(C::kSplitPieces)>> {
   static constexpr bool v = C::kSplitPieces;
 };
-constexpr uint32_t kPiece = 8;     // quads per queued piece
-constexpr uint32_t kPQ = 320;      // queue capacity (a tile holds <= ~2050 quads)
+#ifndef GC_PIECE
+#define GC_PIECE 4
+#endif
+constexpr uint32_t kPiece = GC_PIECE;                // quads per queued piece
+constexpr uint32_t kPQ = 2560 / kPiece;              // queue capacity (a tile holds <= ~2050 quads)
 
 #ifndef GC_DECODE_MINB
 #define GC_DECODE_MINB 3
@@ -516,10 +525,12 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
                   if constexpr (kSplit) {
                     if (jb - ja > kPiece) {
                       jend = ja + kPiece;
-                      for (uint32_t p = jend; p < jb; p += kPiece) {
+                      // one slot reservation for all of the group's pieces
+                      const uint32_t np = (jb - jend + kPiece - 1) / kPiece;
+                      uint32_t slot = oref + 4u * jb < (1u << 14) ? atomicAdd(&s_qn, np) : kPQ;
+                      for (uint32_t p = jend; p < jb; p += kPiece, slot++) {
                         const uint32_t cnt = min(kPiece, jb - p);
                         const uint32_t pos = gd + (p - gq) * g.step, idx = oref + 4u * p;
-                        const uint32_t slot = idx < (1u << 14) ? atomicAdd(&s_qn, 1u) : kPQ;
                         if (slot < kPQ) {
                           s_pq[slot] = make_uint2(pos, idx | (min(n - 4u * p, 32u) << 14) | (cnt << 20) |
                                                            (g.bw << 24));
