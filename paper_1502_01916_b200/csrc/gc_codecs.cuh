@@ -232,18 +232,25 @@ struct CodecGscCU {
   __device__ static WAgg word_agg_fast(const WCtx& c) {
     return WAgg{(uint32_t)__popc(~c.w), (uint32_t)(CG * 32), 0u};
   }
-  // a run of >= 32/CG ones touching this word (stream order, previous word included)
+  // a run of >= 32/CG ones ending in this word (stream order, MSB first; the previous word
+  // of the list included): one inside the word, or the previous word's trailing ones plus
+  // this word's leading ones
   __device__ static bool suspect(const WCtx& c) {
-    uint64_t x = ((uint64_t)(c.widx ? __byte_perm(c.prev, 0, 0x0123) : 0u) << 32) |
-                 __byte_perm(c.w, 0, 0x0123);
-    uint64_t y = x;
+    constexpr uint32_t L = 32u / CG;
+    const uint32_t cur = __byte_perm(c.w, 0, 0x0123);
+    uint32_t y = cur;
     uint32_t have = 1;
-    while (have * 2 <= 32u / CG) {
+#pragma unroll
+    for (int s = 0; s < 5; s++) {
+      if (have * 2 > L) break;
       y &= y >> have;
       have *= 2;
     }
-    if (have < 32u / CG) y &= y >> (32u / CG - have);
-    return (uint32_t)y != 0;
+    if (have < L) y &= y >> (L - have);
+    const uint32_t lead = __clz(~cur);  // leading ones of this word (32 if all ones)
+    const uint32_t prv = c.widx ? __byte_perm(c.prev, 0, 0x0123) : 0u;
+    const uint32_t trail = prv == 0xFFFFFFFFu ? 32u : (uint32_t)(__ffs(~prv) - 1);  // trailing ones
+    return y != 0 || (lead > 0 && lead + trail >= L);
   }
   // the start (stream position relative to the word, negative: in the previous word) of
   // the first code ending in part p; *from_prev: it begins in the previous word
@@ -341,8 +348,10 @@ struct CodecGscIU {
     for (int i = 0; i < 4; i++) {
       uint32_t b = (c.w >> (8 * i)) & 0xFFu;
       if (b == 0xFFu) return true;
+      if (32u / CG >= 8u) continue;  // (a code of > 8 units needs a byte of ones: above)
       uint32_t t = b & (b + 1);  // clear the trailing (padding) ones
       uint32_t y = t;
+#pragma unroll
       for (uint32_t r = 1; r < 32u / CG; r++) y &= t << r;
       if (y & 0xFFu) return true;
     }

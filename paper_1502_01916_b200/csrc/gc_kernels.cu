@@ -274,16 +274,31 @@ __global__ void __launch_bounds__(kThreads, GC_INDEX_MINB) k_index(Dev D) {
   Seg4 agg{0, 0, 0, 0};
   WAgg wa_[CA];
   uint32_t wli[CA];
+  // the current list's first word and length and the next list's first word, reloaded only
+  // when a word crosses into the next list (a thread's 8 words mostly share one list)
+  uint32_t cur_cw = 0, cur_n = 0, next_cw = 0xFFFFFFFFu;
+  if (myn) {
+    cur_cw = cw_at(li);
+    cur_n = n_at(li);
+    next_cw = li + 1 < nl ? cw_at(li + 1) : 0xFFFFFFFFu;
+  }
 #pragma unroll
   for (uint32_t k = 0; k < CA; k++) {
     wa_[k] = WAgg{0, 0, 0};
     wli[k] = li;
     if (k < myn) {
       const uint32_t wr = r0 + k;
-      while (li + 1 < nl && cw_at(li + 1) <= wr) li++;
+      if (next_cw <= wr) {
+        do {
+          li++;
+          cur_cw = next_cw;
+          next_cw = li + 1 < nl ? cw_at(li + 1) : 0xFFFFFFFFu;
+        } while (next_cw <= wr);
+        cur_n = n_at(li);
+      }
       wli[k] = li;
-      const uint32_t widx = wr - cw_at(li);
-      const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, (n_at(li) + 3ull) >> 2, 0u};
+      const uint32_t widx = wr - cur_cw;
+      const WCtx c{wv[k], k ? wv[k - 1] : pw, widx, (cur_n + 3ull) >> 2, 0u};
       const WAgg a = word_agg<C>(c);
       wa_[k] = a;
       agg = widx == 0 ? Seg4{1u, a.q, a.d, a.e} : Seg4{agg.f, agg.q + a.q, agg.d + a.d, agg.e + a.e};
