@@ -518,3 +518,24 @@ def test_library_build_flags():
         assert flags & 1, "GC_LIB does not point at a -DGC_CHECKED build"
     else:
         assert flags in (0, 1, 2, 3)
+
+
+@pytest.mark.parametrize("max_grid", [0, 3])
+def test_afor_piece_queue(max_grid, monkeypatch):
+    """Group-AFOR frames of 8..32 quads are split after the parse into queued 4-quad
+    pieces: frames of every length and width, frames straddling tile edges
+    (lists ending a few ints past multiples of 8192 and 128), lists ending inside a frame's
+    last piece, and runs of gap 1 (32-quad frames at 1 bit) beside wide gaps -- against the
+    oracle, with the whole grid and with 3 CTAs (many tiles per CTA, the queue reused)."""
+    if max_grid:
+        monkeypatch.setenv("GC_DECODE_MAX_GRID", str(max_grid))
+    rng = np.random.default_rng(77)
+    ln = np.array([8192 * 3 + 5, 127, 129, 1, 2, 3, 511, 513, 8190, 4099, 65536 + 17, 33, 96, 97]
+                  + list(rng.integers(1, 3000, 40)), np.uint32)
+    n = int(ln.sum())
+    v = np.ones(n, np.uint32)                              # gap-1 runs: long 1-bit frames
+    wide = rng.random(n) < 0.3
+    v[wide] = rng.integers(1, 1 << 20, int(wide.sum()), dtype=np.uint64).astype(np.uint32)
+    runs = rng.random(n) < 0.02                            # occasional 32-bit outliers
+    v[runs] = rng.integers(1 << 31, 1 << 32, int(runs.sum()), dtype=np.uint64).astype(np.uint32)
+    check(v, ln, O.GROUP_AFOR, 0)
