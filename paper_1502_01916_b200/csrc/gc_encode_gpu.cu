@@ -681,34 +681,49 @@ __global__ void k_afor_dp(Afor A) {  // one thread per list
   const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= A.n_lists) return;
   const uint64_t b0 = A.blk_off[l], S = A.blk_off[l + 1] - b0;
+  // the DP's dependency chain stays in registers: the costs of the next 4 slots (cost of the
+  // rest past the list end = 0) and the block maxima of the next 3 slots slide with s, so a
+  // step waits on no memory round trip (the costs went through global memory before: one L2
+  // round trip per slot, 42.9 ms for config 4's longest lists)
+  uint64_t c1 = 0, c2 = 0, c4a = 0, c4b = 0;  // cost[s+1], cost[s+2], cost[s+3], cost[s+4]
+  uint32_t m1 = 0, m2 = 0, m3 = 0;            // bmax[s+1], bmax[s+2], bmax[s+3]
   for (int64_t s = (int64_t)S - 1; s >= 0; s--) {
+    const uint32_t m0 = A.bmax[b0 + s];
+    const uint64_t left = (uint64_t)S - (uint64_t)s;  // slots from s to the list end
     uint64_t best = ~0ull;
     uint8_t bl = 8;
-    uint32_t bw = 1;
+    uint32_t bw = max(1u, m0), bbw = bw;
+#pragma unroll
     for (uint32_t L = 8; L <= 32; L <<= 1) {  // bw of the first L quads from s
-      if ((uint64_t)s + L / 8 > S) break;
-      for (uint32_t k = (L == 8 ? 0 : L / 16); k < L / 8; k++) bw = max(bw, (uint32_t)A.bmax[b0 + s + k]);
+      if (L / 8 > left) break;
+      if (L == 16) bw = max(bw, m1);
+      if (L == 32) bw = max(bw, max(m2, m3));
       // candidates in the oracle's order 32, 16, 8: evaluate all, pick by that order below
-      const uint64_t rest = (uint64_t)s + L / 8 < S ? A.cost[b0 + s + L / 8] : 0ull;
+      const uint64_t rest = L == 8 ? c1 : (L == 16 ? c2 : c4b);
       const uint64_t c = 8 + 128 * (((uint64_t)L * bw + 31) / 32) + rest;
       // strict improvement in the order 32, 16, 8 == the smallest cost, ties to the longest L
       if (c < best || (c == best && L > bl)) {
         best = c;
         bl = (uint8_t)L;
+        bbw = bw;
       }
     }
-    A.cost[b0 + s] = best;
     A.fstart[b0 + s] = bl;  // (the choice; turned into frame starts below)
+    A.fbw[b0 + s] = (uint8_t)bbw;  // (its width: read back only where a frame starts)
+    c4b = c4a;
+    c4a = c2;
+    c2 = c1;
+    c1 = best;
+    m3 = m2;
+    m2 = m1;
+    m1 = m0;
   }
   // forward: the frames, their bw, vector offsets and indices
   uint64_t f = 0, vec = 0;
   uint64_t s = 0;
   while (s < S) {
-    const uint32_t L = A.fstart[b0 + s];
-    uint32_t bw = 1;
-    for (uint32_t k = 0; k < L / 8; k++) bw = max(bw, (uint32_t)A.bmax[b0 + s + k]);
+    const uint32_t L = A.fstart[b0 + s], bw = A.fbw[b0 + s];
     for (uint32_t k = 1; k < L / 8; k++) A.fstart[b0 + s + k] = 0;
-    A.fbw[b0 + s] = (uint8_t)bw;
     A.fvec[b0 + s] = (uint32_t)vec;
     A.fidx[b0 + s] = (uint32_t)f;
     vec += ((uint64_t)L * bw + 31) / 32;
