@@ -23,7 +23,17 @@
 //      tile's first list start after the look-back.
 
 __host__ __device__ constexpr uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
-constexpr uint32_t kHalo = 32;                     // staging index = tile position + kHalo
+// Tile stores by TMA (cp.async.bulk.tensor, 128-byte swizzle; -DGC_TMA_STORE=1): the staging
+// window's swizzle (below) is the TMA's SWIZZLE_128B pattern when the window is 1024-byte
+// aligned, so boxes of 8 rows x 32 ints leave straight from it.  The halo is then one whole
+// 1 KiB swizzle atom, so every box starts 1024-byte aligned.  Correct (the GPU suite passes
+// with it) but 1-2% slower than the 128-bit stores, so off by default.
+#ifndef GC_TMA_STORE
+#define GC_TMA_STORE 0
+#endif
+constexpr bool kTma = GC_TMA_STORE != 0;
+constexpr uint32_t kHalo = kTma ? 256 : 32;        // staging index = tile position + kHalo
+constexpr uint32_t kBoxC = 64;                     // 16-B chunks per TMA store box (8 rows of 32 ints)
 constexpr uint32_t kStW = kHalo + kT + 8;          // staging ints
 // Staging capacities of a codec.  Frame codecs (PFD, SIMD-BP128) need one control word
 // per 4F ints (a tile spans <= 66), so their control staging is small and the space goes to
@@ -131,16 +141,21 @@ constexpr uint32_t kPQ = 2560 / kPiece;              // queue capacity (a tile h
 // store's docIDs (batch 0, d-gap scan) and term frequencies (batch 1, raw) -- their tiles
 // interleaved (virtual tile 2t = docIDs tile t, 2t+1 = TFs tile t): one launch, the same
 // CTAs, the TF tiles' unpack filling the docID tiles' look-back latency.
+// tm0 / tm1: 2-D tensor maps of out0 / out1 ({32 ints, total_out / 32 rows}, boxes of 8 rows,
+// 128-byte swizzle); bit b of tma says tm<b> is valid (else plain 128-bit stores).
 template <class C, bool DGAPS, bool PAIR = false>
 __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t* __restrict__ out0,
-                                                                Dev D1, uint32_t* __restrict__ out1) {
+                                                                Dev D1, uint32_t* __restrict__ out1,
+                                                                const __grid_constant__ CUtensorMap tm0,
+                                                                const __grid_constant__ CUtensorMap tm1,
+                                                                uint32_t tma) {
   const Dev& D = D0;       // (the docIDs batch: the look-back and the deferred carry stores)
   uint32_t* out = out0;
   // virtual tile vt -> its batch and its tile index in that batch
   auto bat = [&](uint32_t vt) -> const Dev& { return (PAIR && (vt & 1u)) ? D1 : D0; };
   auto tix = [&](uint32_t vt) { return PAIR ? vt >> 1 : vt; };
   const uint32_t nvt = PAIR ? 2 * D0.n_tiles_b : D0.n_tiles_b;
-  extern __shared__ __align__(128) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm[];
   uint32_t* s_out = reinterpret_cast<uint32_t*>(sm + DS<C>::kOut);
   uint4* s_out4 = reinterpret_cast<uint4*>(sm + DS<C>::kOut);
   uint4* s_data = reinterpret_cast<uint4*>(sm + DS<C>::kData);
@@ -164,6 +179,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
   __shared__ uint32_t s_reset0[2], s_cin;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!kTma || (smem_addr(sm) & 1023u) != 0) tma = 0;  // (the swizzle atoms must be aligned)
   constexpr uint32_t kU = UnitsPerThread<C>::v;  // parse units per thread per parse chunk
   uint32_t phase = 0, err = 0;
 
@@ -337,6 +353,8 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
     uint32_t* const out = (PAIR && (vt & 1u)) ? out1 : out0;
     const uint32_t tile = tix(vt);
     const bool dg = DGAPS && !(PAIR && (vt & 1u));    // (TFs: no d-gap)
+    const bool use_tma = (tma >> ((PAIR && (vt & 1u)) ? 1 : 0)) & 1u;
+    const CUtensorMap* tm = (PAIR && (vt & 1u)) ? &tm1 : &tm0;
     // warp 1 prefetches the next tile's entries (read after this tile's unpack)
     if (warp == 1) load_entries(vt + gridDim.x);
     if (tid == 0) s_reset0[buf ^ 1u] = kT;  // the next tile's
@@ -440,6 +458,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
         mbar_wait(&s_bar[0], phase);
         w0done = true;
       }
+      if (kTma && warp == 0) bulk_wait_read0();  // the previous tile's TMA stores have read staging
       __syncthreads();
       GC_T(1);
       const uint32_t rw0 = lr == 0 ? rwa : lt_cw[0];
@@ -610,6 +629,8 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
       else pieces(std::false_type{});
     }
     if (DGAPS && s_pend.on) flush_pending();  // (a tile that staged nothing)
+    if (kTma && warp == 0) bulk_wait_read0();  // (a tile without list rounds)
+    if (kTma && !dg) fence_proxy_async_smem();  // the staged ints are read by the TMA stores
     __syncthreads();  // the tile is staged; the staging buffers and the next entries are free
     // the next tile's copies overlap this tile's scan, look-back and stores
     if (tid == 0) {
@@ -660,6 +681,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
 #pragma unroll
       for (uint32_t a = 0; a < 8; a++)
         s_out4[sw_chunk(cb + a)] = make_uint4(v[4 * a], v[4 * a + 1], v[4 * a + 2], v[4 * a + 3]);
+      if (kTma) fence_proxy_async_smem();  // the scanned ints are read by the TMA stores
       if (tid == 0)
         st_relaxed_u64(D.tiles_b + tile, ((uint64_t)(rcarry.f ? kFlagIncl : kFlagAgg) << 32) | rcarry.v);
       __syncthreads();
@@ -696,6 +718,23 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
         __stcs(o4 + c, s_out4[sw_chunk(kHalo / 4 + c)]);
       }
     };
+    // chunks [c0, nch), no carry: whole 8-row boxes by TMA (lane b of warp 0 issues box b),
+    // the rest by 128-bit stores
+    auto store_from = [&](uint32_t c0) {
+      const uint32_t full = nvalid >> 2;
+      const uint32_t b0 = (c0 + kBoxC - 1) / kBoxC, b1 = full / kBoxC;
+      if (kTma && use_tma && b1 > b0) {
+        if (warp == 0 && lane >= b0 && lane < b1) {
+          tma_store_2d(tm, s_out + kHalo + lane * (kBoxC * 4), 0, (int32_t)((tT >> 5) + lane * 8));
+          bulk_commit();
+        }
+        store_plain(c0, b0 * kBoxC);
+        store_plain(b1 * kBoxC, full);
+      } else {
+        store_plain(c0, full);
+      }
+      for (uint32_t c = max(c0, full) + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
+    };
     if (dg) {
       const uint32_t reset0 = s_reset0[buf];
 #ifdef GC_ABL_NOFLUSH
@@ -704,8 +743,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
       const bool need_carry = ok && reset0 != 0u;  // the tile's first int continues a list
 #endif
       const uint32_t cfree = need_carry ? min(nch, (reset0 + 3u) / 4u) : 0u;
-      store_plain(cfree, nvalid >> 2);
-      for (uint32_t c = max(cfree, nvalid >> 2) + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
+      store_from(cfree);
       if (need_carry && tid == 0) {
         s_pend.on = 1;
         s_pend.tile = tile;
@@ -718,13 +756,13 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
       }
       GC_T(6);
     } else {
-      store_plain(0u, nvalid >> 2);
-      for (uint32_t c = (nvalid >> 2) + tid; c < nch; c += kDT) store_chunk(c, 0u, 0u);
+      store_from(0u);
     }
     __syncthreads();  // staging window, bitmap and the next tile's geometry settled
     GC_T(7);
   }
   if (DGAPS && s_pend.on) flush_pending();
+  if (kTma && warp == 0) bulk_wait0();  // the TMA stores are done with shared memory
   err = __reduce_or_sync(0xffffffffu, err);
   if (lane == 0 && err) atomicOr(&D.hdr->status, err);
 }

@@ -193,6 +193,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
+// Tensor bulk async store shared -> global (TMA engine, SASS UTMASTG): one box of the 2-D
+// tensor map tm at coordinates (c0 inner, c1 outer), tracked by the issuing thread's bulk
+// groups.  The source's writers fence (fence.proxy.async.shared::cta) before the barrier
+// that precedes the issue; the issuer waits for the reads (wait_group.read) before the
+// buffer is written again.
+__device__ __forceinline__ void tma_store_2d(const void* tm, const void* src_smem, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm),
+               "r"(smem_addr(src_smem)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

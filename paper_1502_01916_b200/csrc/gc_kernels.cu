@@ -16,11 +16,14 @@
 //      Group-PFD exceptions in shared memory, runs the segmented d-gap inclusive
 //      scan (thread-serial + block + decoupled look-back across tiles) and writes
 //      the tile with coalesced 128-bit stores.
+#include <cuda.h>  // CUtensorMap (the decode's TMA tile stores)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 #include "gc.h"
@@ -962,6 +965,40 @@ gc_status launch_index(const Dev& D, cudaStream_t st, const DevInfo& di) {
   return cudaGetLastError() == cudaSuccess ? GC_OK : GC_ERR_CUDA;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).  The
+// pointer is process-wide and device-independent; std::call_once makes the lookup reentrant.
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+  static std::once_flag once;
+  static EncodeTiled fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+// The decode output as a 2-D tensor {32 ints, total_out / 32 rows} with 8-row boxes and the
+// staging window's 128-byte swizzle (gc_decode.cuh).  False (plain stores) when the output is
+// not 16-byte aligned, shorter than a row, or the encoder is unavailable.
+bool out_tensor_map(CUtensorMap* tm, uint32_t* out, uint64_t total_out) {
+  memset(tm, 0, sizeof(*tm));
+  const EncodeTiled enc = encode_tiled();
+  const uint64_t rows = total_out / 32;
+  if (!kTma || !enc || rows == 0 || ((uintptr_t)out & 15u) || rows > (1ull << 31)) return false;
+  const cuuint64_t dims[2] = {32, rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, kBoxC / 8};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // k_decode over one batch, or (pair) over a docIDs batch D and a TFs batch *D1 together
 template <class C>
 gc_status launch_decode(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st, const DevInfo& di,
@@ -990,7 +1027,11 @@ gc_status launch_decode(const Dev& D, uint32_t* out, bool dgaps, cudaStream_t st
   const unsigned grid = (unsigned)mn64(nvt, cap);
   Dev Dv = D, Dv1 = D1 ? *D1 : D;
   uint32_t* o1 = D1 ? out1 : out;
-  void* args[] = {&Dv, &out, &Dv1, &o1};
+  alignas(64) CUtensorMap tm0, tm1;
+  uint32_t tma = out_tensor_map(&tm0, out, D.total_out) ? 1u : 0u;
+  if (D1 && out_tensor_map(&tm1, out1, D1->total_out)) tma |= 2u;
+  if (!D1) tm1 = tm0;
+  void* args[] = {&Dv, &out, &Dv1, &o1, &tm0, &tm1, &tma};
   if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kDT), args, smem, st) !=
       cudaSuccess)
     return GC_ERR_CUDA;
