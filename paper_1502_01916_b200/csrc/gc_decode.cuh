@@ -32,6 +32,11 @@ __host__ __device__ constexpr uint32_t al128(uint32_t x) { return (x + 127u) & ~
 #define GC_TMA_STORE 0
 #endif
 constexpr bool kTma = GC_TMA_STORE != 0;
+// Software-pipelined unpack of the one-quad-per-group codecs (-DGC_PIPE=1): see units().
+#ifndef GC_PIPE
+#define GC_PIPE 0
+#endif
+constexpr bool kPipe = GC_PIPE != 0;
 constexpr uint32_t kHalo = kTma ? 256 : 32;        // staging index = tile position + kHalo
 constexpr uint32_t kBoxC = 64;                     // 16-B chunks per TMA store box (8 rows of 32 ints)
 constexpr uint32_t kStW = kHalo + kT + 8;          // staging ints
@@ -389,12 +394,10 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
     const uint64_t lb = la + nl - 1;
     bool w0done = false, w1done = false;
 
-    // one quad: 4 values of BW bits at data lane-bit pos; their ints go to staging
-    // indices idx .. idx + min(4, rem) - 1
-    auto unpack_quad = [&](uint32_t pos, uint32_t bw, uint32_t idx, uint32_t rem, auto staged) {
+    // the two data vectors of a quad at data lane-bit pos
+    auto load_quad = [&](uint32_t pos, uint4& v0, uint4& v1, auto staged) {
       constexpr bool kStaged = decltype(staged)::value;
-      const uint32_t m = min(pos >> 5, dlim - 1u), off = pos & 31u;
-      uint4 v0, v1;
+      const uint32_t m = min(pos >> 5, dlim - 1u);
       if constexpr (kStaged) {
         GC_CHECK(m + 1 <= DS<C>::kDC);
         v0 = s_data[m];
@@ -404,6 +407,11 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
         v0 = __ldg(D.data + va + m);
         v1 = __ldg(D.data + va + min(m + 1, dlim - 1u));
       }
+    };
+    // 4 values of BW bits at bit `off` of v0 (continued in v1) to staging indices idx ..
+    // idx + min(4, rem) - 1
+    auto stage_quad = [&](const uint4& v0, const uint4& v1, uint32_t off, uint32_t bw, uint32_t idx,
+                          uint32_t rem) {
       // the value's high part is the top of the current component, its low part the
       // bottom of the next vector's component
       const bool strad = off + bw > 32u;
@@ -425,6 +433,13 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
         s_out[rem > 2u ? sw_word(idx + 2) : 1u] = x2;
         s_out[rem > 3u ? sw_word(idx + 3) : 2u] = x3;
       }
+    };
+    // one quad: 4 values of BW bits at data lane-bit pos; their ints go to staging
+    // indices idx .. idx + min(4, rem) - 1
+    auto unpack_quad = [&](uint32_t pos, uint32_t bw, uint32_t idx, uint32_t rem, auto staged) {
+      uint4 v0, v1;
+      load_quad(pos, v0, v1, staged);
+      stage_quad(v0, v1, pos & 31u, bw, idx, rem);
     };
 
     for (uint64_t lr = 0; lr < nl; lr += kLC) {
@@ -516,6 +531,9 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
           w1done = true;
         }
         auto units = [&](auto staged) {
+          uint4 p_v0 = make_uint4(0u, 0u, 0u, 0u), p_v1 = p_v0;  // (kPipe) the quad in flight
+          uint32_t p_off = 0, p_bw = 0, p_idx = 0, p_rem = 0;
+          bool p_have = false;
 #pragma unroll
           for (uint32_t k = 0; k < kU; k++) {
             if (k >= myn) break;
@@ -528,7 +546,24 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
             if (qb > qa) {
               const WCtx c{wv[k], pv[k], widx, lt_q[i], part};
               const uint32_t n = lt_n[i], oref = lt_oref[i];
-              if constexpr (!C::kMultiQuad) {
+              if constexpr (!C::kMultiQuad && kPipe) {
+                // one quad per group, software-pipelined: a quad's vectors are loaded before
+                // the previous quad is shifted, masked and staged, so the shared-memory load
+                // latency overlaps that work (the compiler cannot move the loads above the
+                // staging stores itself: both are shared memory)
+                C::emit(c, S.q, S.d, qa, qb, [&](uint32_t j, uint32_t pos, uint32_t bw) {
+                  uint4 v0, v1;
+                  load_quad(pos, v0, v1, staged);
+                  if (p_have) stage_quad(p_v0, p_v1, p_off, p_bw, p_idx, p_rem);
+                  p_v0 = v0;
+                  p_v1 = v1;
+                  p_off = pos & 31u;
+                  p_bw = bw;
+                  p_idx = oref + 4u * j;
+                  p_rem = n - 4u * j;
+                  p_have = true;
+                });
+              } else if constexpr (!C::kMultiQuad) {
                 // one quad per group: the codec's tight loop straight into the unpack
                 C::emit(c, S.q, S.d, qa, qb, [&](uint32_t j, uint32_t pos, uint32_t bw) {
                   unpack_quad(pos, bw, oref + 4u * j, n - 4u * j, staged);
@@ -600,6 +635,7 @@ __global__ void __launch_bounds__(kDT, GC_DECODE_MINB) k_decode(Dev D0, uint32_t
             S.d += a.d;
             S.e += a.e;
           }
+          if (kPipe && p_have) stage_quad(p_v0, p_v1, p_off, p_bw, p_idx, p_rem);
         };
         if (DGAPS && s_pend.on) {  // (uniform: s_pend.on only changes behind barriers)
           GC_T(3);
